@@ -1,0 +1,158 @@
+"""Seeded synthetic inputs: the generators and the five BASELINE configs.
+
+Host-side input preparation (the reference excludes it from every timing).
+The generators restate the reference's published recipes so the GPU box can
+rebuild bit-identical inputs without /root/reference:
+
+* R-MAT, one quadrant draw per bit (pkg/src/maskmul/generate.py:52-65,
+  Graph500 (a,b,c,d) = (0.57, 0.19, 0.19, 0.05), :16)
+* Erdős–Rényi pairs with replacement (generate.py:68-73)
+* duplicates merged, unit values (generate.py:76-88)
+
+Config recipes are SURVEY.md §8(d); tests/golden/configs.json pins every
+generated input by digest against the reference's own generator output.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .semiring import arithmetic_semiring, plus_pair_semiring
+from .sparse import (CsrMatrix, degree_sort_relabel, from_arrays,
+                     simple_undirected_graph, tril_strict)
+
+GRAPH500_PARAMS = (0.57, 0.19, 0.19, 0.05)
+
+
+@dataclass(frozen=True)
+class GeneratorSpec:
+    kind: str
+    scale: int
+    avg_degree: float
+    rmat_params: tuple = GRAPH500_PARAMS
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.kind not in ("erdos-renyi", "rmat"):
+            raise ValueError(f"unknown generator kind {self.kind!r}")
+        if self.scale < 1:
+            raise ValueError("scale must be >= 1")
+        if not self.avg_degree > 0:
+            raise ValueError("avg_degree must be > 0")
+        if abs(sum(self.rmat_params) - 1.0) > 1e-9:
+            raise ValueError("rmat_params must sum to 1 within 1e-9")
+
+    @property
+    def nrows(self) -> int:
+        return 1 << self.scale
+
+    @property
+    def nedges(self) -> int:
+        return int(round(self.avg_degree * self.nrows))
+
+
+def rmat_edges(spec: GeneratorSpec):
+    a, b, c, _ = spec.rmat_params
+    cuts = np.array([a, a + b, a + b + c])
+    rng = np.random.default_rng(spec.seed)
+    m = spec.nedges
+    src = np.zeros(m, dtype=np.int64)
+    dst = np.zeros(m, dtype=np.int64)
+    for bit in range(spec.scale):
+        quad = np.searchsorted(cuts, rng.random(m), side="right")
+        src |= (quad >> 1).astype(np.int64) << bit
+        dst |= (quad & 1).astype(np.int64) << bit
+    return src, dst
+
+
+def erdos_renyi_edges(spec: GeneratorSpec):
+    rng = np.random.default_rng(spec.seed)
+    n = spec.nrows
+    src = rng.integers(0, n, spec.nedges, dtype=np.int64)
+    dst = rng.integers(0, n, spec.nedges, dtype=np.int64)
+    return src, dst
+
+
+def generate(spec: GeneratorSpec) -> CsrMatrix:
+    src, dst = rmat_edges(spec) if spec.kind == "rmat" else erdos_renyi_edges(spec)
+    n = spec.nrows
+    key = np.unique(src * np.int64(n) + dst)
+    rows = key // n
+    cols = key - rows * n
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    row_ptr[1:] = np.cumsum(np.bincount(rows, minlength=n))
+    return CsrMatrix(n, n, row_ptr, cols, np.ones(key.size, dtype=np.int64))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configs
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Workload:
+    name: str
+    mask: object          # MaskView
+    a: CsrMatrix
+    b: CsrMatrix
+    semiring: object
+    complemented: bool
+    description: str
+
+
+def cfg1() -> Workload:
+    a = generate(GeneratorSpec("erdos-renyi", 12, 8, seed=0)).astype(np.float64)
+    a.values[:] = np.random.default_rng(1).random(a.nnz)
+    return Workload("cfg1", a.pattern(), a, a, arithmetic_semiring(np.float64), False,
+                    "ER n=4096 d8, M=A=B, fp64 U(0,1), plus-times")
+
+
+def triangle_lower(scale: int = 20, degree: float = 16, seed: int = 0) -> CsrMatrix:
+    g = simple_undirected_graph(generate(GeneratorSpec("rmat", scale, degree, seed=seed)))
+    return tril_strict(degree_sort_relabel(g)[0])
+
+
+def cfg2(scale: int = 20) -> Workload:
+    low = triangle_lower(scale)
+    return Workload("cfg2", low.pattern(), low, low, plus_pair_semiring(np.int64), False,
+                    f"triangle count R-MAT s{scale} ef16, L=tril(relabel(G)), C=L.(L L) plus-pair")
+
+
+def cfg3(mask_degree: int) -> Workload:
+    a = generate(GeneratorSpec("erdos-renyi", 18, 16, seed=0)).astype(np.float64)
+    a.values[:] = np.random.default_rng(100).random(a.nnz)
+    b = generate(GeneratorSpec("erdos-renyi", 18, 16, seed=1)).astype(np.float64)
+    b.values[:] = np.random.default_rng(101).random(b.nnz)
+    m = generate(GeneratorSpec("erdos-renyi", 18, mask_degree, seed=2))
+    return Workload(f"cfg3_d{mask_degree}", m.pattern(), a, b, arithmetic_semiring(np.float64),
+                    False, f"ER 2^18 d16 fp64, mask d={mask_degree}")
+
+
+def cfg4() -> Workload:
+    g = simple_undirected_graph(generate(GeneratorSpec("rmat", 18, 16, seed=0)))
+    n = g.nrows
+    rng = np.random.default_rng(4)
+    src = rng.choice(n, 512, replace=False)
+    ft = from_arrays(512, n, np.arange(512), src, np.ones(512, dtype=np.int64))
+    # V = (rng.random((512, n)) < 0.05), drawn row block by row block to
+    # bound host memory; the PCG64 double stream is consumed in the same order
+    rows_l, cols_l = [], []
+    for r0 in range(0, 512, 64):
+        blk = rng.random((64, n)) < 0.05
+        r, c = np.nonzero(blk)
+        rows_l.append(r + r0)
+        cols_l.append(c)
+    rows = np.concatenate(rows_l)
+    cols = np.concatenate(cols_l)
+    row_ptr = np.zeros(513, dtype=np.int64)
+    row_ptr[1:] = np.cumsum(np.bincount(rows, minlength=512))
+    v = CsrMatrix(512, n, row_ptr, cols.astype(np.int64), np.ones(cols.size, dtype=np.int64))
+    return Workload("cfg4", v.pattern(complemented=True), ft, g, arithmetic_semiring(np.int64),
+                    True, "BFS step C = not(V) . (F^T A), 512 sources, R-MAT s18, int64")
+
+
+def cfg5(scale: int = 22) -> Workload:
+    g = simple_undirected_graph(generate(GeneratorSpec("rmat", scale, 16, seed=0)))
+    return Workload("cfg5", g.pattern(), g, g, plus_pair_semiring(np.int64), False,
+                    f"k-truss support R-MAT s{scale} ef16, C=A.(A A) plus-pair")
