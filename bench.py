@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark: masked SpGEMM triangle count (BASELINE config 2) on B200.
+
+Workload (BASELINE.json configs[1]): R-MAT scale 20, edge factor 16, Graph500
+(a,b,c,d), symmetrised, self loops / duplicates removed, relabelled by
+non-increasing degree, L = strict lower triangle; C = L (.) (L L) under the
+plus-pair semiring with int64 counts; sum(C) = triangles (423,909,251).
+
+A "step" is one full masked multiply through the library (row analysis,
+binning, numeric kernels, row-pointer scan, nnz readback, exact-size C,
+compaction) plus the device reduction of sum(C).  Inputs are resident in HBM
+when the timed region starts (`value`); `e2e` repeats the step through the
+public API from pinned HOST buffers with the host->device copies and the
+device->host read of the triangle count inside the timed region.
+
+    python bench.py [--gpus N --steps K --warmup W]       # ours (default)
+    python bench.py --impl reference                      # CPU oracle arm
+
+N > 1 (torchrun, one process per GPU): A and M are row-blocked by balanced
+work, B is broadcast from rank 0 over NCCL, the per-rank triangle sums are
+all-reduced; total work is fixed, so scaling is "strong".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "masked-SpGEMM useful GFLOP/s & triangles/s; HBM GB/s vs roofline at 1/2/4/8 B200"
+UNIT = "useful GFLOP/s"
+EXPECTED_TRIANGLES = {20: 423909251}
+SUMMARY_BYTES = 184          # sizeof(mm::Summary), read back twice per multiply
+L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algo", default="hash")
+    ap.add_argument("--scale", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def push_bytes(m, nnz_a, flops, nnz_m, nnz_c, v):
+    """SURVEY.md §8(d) algorithmic bytes of the push path (v = value bytes)."""
+    return (8 * (m + 1) + nnz_a * (4 + v) + 16 * nnz_a + flops * (4 + v)
+            + 8 * (m + 1) + 4 * nnz_m + 8 * (m + 1) + 12 * nnz_c)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_inputs(scale):
+    from paper_2111_09947_b200 import workloads
+    t0 = time.perf_counter()
+    low = workloads.triangle_lower(scale)
+    return low, time.perf_counter() - t0
+
+
+def cpu_reference_run(low, workers, rows=None):
+    """Oracle (C restatement of the reference, MSA-1P) on all rows or a row block."""
+    import numpy as np
+
+    import oracle
+    from paper_2111_09947_b200.sparse import CsrMatrix
+    a = low
+    if rows is not None:
+        lo, hi = rows
+        p0, p1 = int(low.row_ptr[lo]), int(low.row_ptr[hi])
+        a = CsrMatrix(hi - lo, low.ncols, low.row_ptr[lo:hi + 1] - p0, low.col_idx[p0:p1],
+                      low.values[p0:p1])
+    r = oracle.masked_multiply(a.pattern(), a, low, algorithm="msa", semiring_id=1,
+                               dtype=np.int64, workers=workers)
+    return r
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.load()
+    low, _ = build_inputs(args.scale)
+    workers = oracle.max_threads()
+    # bound the run to a few minutes: sample a row block if the full multiply is slow
+    t0 = time.perf_counter()
+    r = cpu_reference_run(low, workers)
+    t_full = time.perf_counter() - t0
+    budget = 150.0
+    rows = None
+    sample = f"full workload (all {low.nrows} rows), MSA-1P"
+    if t_full * (args.steps + args.warmup) > budget:
+        frac = max(0.01, budget / ((args.steps + args.warmup) * t_full))
+        # rows are heavy at low ids (hubs first): take an interleaved-free prefix
+        # block holding ~frac of the work
+        import numpy as np
+        from paper_2111_09947_b200.distributed import row_work
+        w = row_work(low.row_ptr, low.col_idx, low.row_ptr, low.row_ptr)
+        cum = np.cumsum(w)
+        hi = int(np.searchsorted(cum, frac * cum[-1])) + 1
+        rows = (0, min(hi, low.nrows))
+        sample = f"rows [0, {rows[1]}) of {low.nrows} (~{frac:.0%} of the work), MSA-1P"
+    for _ in range(max(args.warmup - 1, 0)):
+        cpu_reference_run(low, workers, rows)
+    times, evals = [], []
+    for _ in range(args.steps):
+        r = cpu_reference_run(low, workers, rows)
+        times.append(r.total_seconds)
+        evals.append(r.evaluated_multiplies)
+    t = sum(times) / len(times)
+    value = evals[0] / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (seeded R-MAT, reference generator restated)",
+        "config": {"workload": f"cfg2 triangle count R-MAT s{args.scale} ef16, L.(L L) plus-pair int64",
+                   "parallelism": f"cpu threads x{workers}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "triangles_per_s": (evals[0] / t) if rows is None else None,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_09947_b200 import MultiplyPlan, plus_pair_semiring
+    from paper_2111_09947_b200 import _lib
+    from paper_2111_09947_b200.device import DeviceCsr
+    from paper_2111_09947_b200.distributed import (allreduce_sum_, balanced_cuts, broadcast_csr,
+                                                   row_block, row_work)
+    from paper_2111_09947_b200.multiply import _handle, multiply_device, reduce_sum
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    low, t_gen = build_inputs(args.scale)
+    m = low.nrows
+    plan = MultiplyPlan(algorithm=args.algo, semiring=plus_pair_semiring(np.int64))
+
+    # host copies (pinned) for e2e; device-resident copies for `value`
+    h_ptr = torch.from_numpy(np.ascontiguousarray(low.row_ptr, dtype=np.int64)).pin_memory()
+    h_idx = torch.from_numpy(np.ascontiguousarray(low.col_idx[: low.nnz], dtype=np.int32)).pin_memory()
+    full = DeviceCsr(m, low.ncols, h_ptr.to(dev), h_idx.to(dev), None)
+    if world > 1:
+        cuts = balanced_cuts(row_work(low.row_ptr, low.col_idx, low.row_ptr, low.row_ptr), world)
+        lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+        b_full = broadcast_csr(full if rank == 0 else None, 0, dev)
+    else:
+        lo, hi = 0, m
+        b_full = full
+    a_blk = row_block(full, lo, hi) if world > 1 else full
+    bt = b_full.transpose_storage() if args.algo in ("inner", "auto") else None
+    stream = torch.cuda.current_stream(dev)
+    lib = _lib.load()
+    import ctypes as C
+    h = _handle(local_rank)
+    lib.mm_profile_enable(h, 1)
+
+    def step(a, b, btt):
+        c, st = multiply_device(a, a, b, plan, b_csc=btt, stream=stream)
+        tri = reduce_sum(c.values) if c.nnz else torch.zeros(1, dtype=torch.int64, device=dev)
+        if world > 1:
+            allreduce_sum_(tri)
+        return c, st, tri
+
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    for w in range(args.warmup):
+        c, st, tri = step(a_blk, b_full, bt)
+    torch.cuda.synchronize()
+    tri_total = int(tri.item())
+    expected = EXPECTED_TRIANGLES.get(args.scale)
+
+    ms_buf = (C.c_float * 6)()
+    launches = C.c_int64(0)
+    phase = [0.0] * 6
+    step_ms = []
+    clocks = ClockSampler(local_rank)
+    n_launch_total = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t_wall0 = time.perf_counter()
+    for s in range(args.steps):
+        flush.fill_(s & 0xFF)                       # evict L2 between timed steps
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c, st, tri = step(a_blk, b_full, bt)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        lib.mm_profile_read(h, ms_buf, 6, C.byref(launches))
+        for q in range(6):
+            phase[q] += ms_buf[q]
+        n_launch_total += int(launches.value) + 2          # + the 2 reduction kernels
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    tri_total = int(tri.item())
+    my_ms = sum(step_ms) / len(step_ms)
+    evaluated_local = st.evaluated_multiplies
+    flops_local = st.generated_flops
+    nnz_c_local = c.nnz
+    if world > 1:
+        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        tot = torch.tensor([evaluated_local, flops_local, nnz_c_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(tot)
+        evaluated, flops, nnz_c = (int(x) for x in tot.tolist())
+    else:
+        ms_max, evaluated, flops, nnz_c = my_ms, evaluated_local, flops_local, nnz_c_local
+    per = [p / args.steps for p in phase]
+
+    # ---- e2e through the public API from pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms = []
+        for s in range(args.steps + 1):
+            flush.fill_(s & 0xFF)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            d_ptr = h_ptr.to(dev, non_blocking=True)
+            d_idx = h_idx.to(dev, non_blocking=True)
+            d_full = DeviceCsr(m, low.ncols, d_ptr, d_idx, None)
+            d_a = row_block(d_full, lo, hi) if world > 1 else d_full
+            d_bt = d_full.transpose_storage() if args.algo in ("inner", "auto") else None
+            _, _, tri_e = step(d_a, d_full, d_bt)
+            tri_host = int(tri_e.item())                   # device->host read of the result
+            e1.record(stream)
+            e1.synchronize()
+            wall = (time.perf_counter() - t0) * 1e3
+            if s > 0:
+                e2e_ms.append(max(e0.elapsed_time(e1), 0.0) if world == 1 else wall)
+            assert tri_host == tri_total
+        e2e_t = sum(e2e_ms) / len(e2e_ms)
+        if world > 1:
+            t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = float(t.item())
+        h2d = h_ptr.numel() * 8 + h_idx.numel() * 4
+        e2e = {"value": evaluated / (e2e_t * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 + 2 * SUMMARY_BYTES,
+               "ms_per_step": e2e_t}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        workers = oracle.max_threads()
+        r = cpu_reference_run(low, workers)
+        t1 = time.perf_counter()
+        r = cpu_reference_run(low, workers)
+        cpu_t = r.total_seconds
+        cpu = {"value": r.evaluated_multiplies / cpu_t / 1e9, "unit": UNIT, "cores": workers,
+               "kind": "port", "seconds": cpu_t,
+               "sample": "full workload, oracle MSA-1P (C restatement of the reference numba "
+                         "kernels), best of 2"}
+        del t1
+
+    if rank == 0:
+        peak, peak_src = measured_peak()
+        nnz_a = low.nnz
+        bytes_alg = push_bytes(m, nnz_a, flops, nnz_a, nnz_c, 0)
+        numeric_ms = per[2]
+        achieved = bytes_alg / (numeric_ms * 1e-3) / 1e9
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tfile):
+            try:
+                with open(tfile) as f:
+                    traffic = json.load(f).get("numeric_bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC,
+            "value": evaluated / (ms_max * 1e-3) / 1e9,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "int64",
+            "data": "synthetic (seeded R-MAT, reference generator restated; inputs pinned by digest)",
+            "config": {"workload": f"cfg2 triangle count R-MAT s{args.scale} ef16, C = L.(L L) plus-pair int64",
+                       "algorithm": plan.label(), "nrows": m, "nnz_L": nnz_a,
+                       "generated_flops": flops, "useful_products": evaluated, "nnz_C": nnz_c,
+                       "triangles": tri_total,
+                       "triangles_ok": (tri_total == expected) if expected else None,
+                       "l2": "flushed (512 MiB write) before every timed step; inputs 71 MB < L2",
+                       "parallelism": f"row-block x{world}" if world > 1 else "1 GPU"},
+            "triangles_per_s": tri_total / (ms_max * 1e-3),
+            "hbm_alg_gbs": bytes_alg / (ms_max * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "push numeric (hash tiers, all bins of one multiply)",
+                         "bytes_alg_per_launch": bytes_alg, "kernel_ms": numeric_ms,
+                         "peak_source": peak_src,
+                         "step_frac": bytes_alg / (ms_max * 1e-3) / 1e9 / peak},
+            "phase_ms": {"analyze": per[0], "scatter": per[1], "numeric": per[2],
+                         "scan_readback": per[3], "compact": per[4], "multiply_total": per[5]},
+            "gpu_launches": n_launch_total,
+            "clocks": clk,
+            "wall_s_timed": t_wall,
+            "input_gen_s": t_gen,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

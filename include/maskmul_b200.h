@@ -1,0 +1,166 @@
+/*
+ * maskmul_b200 — C ABI of the B200-native masked SpGEMM
+ *
+ *     C = M (.) (A B)        and        C = (not M) (.) (A B)
+ *
+ * over the plus-times / plus-pair semirings with int64 or float64 values.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (arxiv 2111.09947, package `maskmul`) has no native FFI: its driver
+ * `masked_multiply_with_stats` (pkg/src/maskmul/multiply.py:349-403) calls
+ * numba-compiled row-chunk kernels (pkg/src/maskmul/_kernels.py:30-594)
+ * through the internal signature
+ *     <algo>_numeric(lo, hi, a_ptr, a_idx, a_val, b_ptr, b_idx, b_val,
+ *                    m_ptr, m_idx, comp, sr, one, <scratch>, out_off,
+ *                    out_idx, out_val, row_nnz) -> evaluated
+ * Each entry point below names the reference function it replaces.  All
+ * pointers in mm_matrix_t are DEVICE pointers (cudaMalloc / torch CUDA
+ * tensors); every call is ordered on the caller's stream (cudaStream_t passed
+ * as void*).  No torch types cross this boundary.
+ *
+ * Status codes mirror the reference's error classes and CLI exit codes
+ * (cli.py:387-410): 0 ok, 1 PlanError, 2 SparseError (shape / input),
+ * 3 internal bound violation (the reference's assertions at
+ * multiply.py:375,390), 4 CUDA error.  mm_last_error() returns a thread-local
+ * message for the last non-zero status.
+ */
+#ifndef MASKMUL_B200_H
+#define MASKMUL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MM_ABI_VERSION 1
+
+/* algorithms: multiply.py:35 ALGORITHMS, plus MM_ALGO_AUTO (per-row push/pull cost model) */
+enum {
+    MM_ALGO_MSA = 0,
+    MM_ALGO_HASH = 1,
+    MM_ALGO_MCA = 2,
+    MM_ALGO_HEAP = 3,
+    MM_ALGO_HEAPDOT = 4,
+    MM_ALGO_INNER = 5,
+    MM_ALGO_AUTO = 6
+};
+
+enum { MM_OK = 0, MM_ERR_PLAN = 1, MM_ERR_INPUT = 2, MM_ERR_INTERNAL = 3, MM_ERR_CUDA = 4 };
+
+/* semiring.py:23-24 kernel_id */
+enum { MM_SR_ARITHMETIC = 0, MM_SR_PLUS_PAIR = 1 };
+enum { MM_DTYPE_INT64 = 0, MM_DTYPE_FLOAT64 = 1 };
+
+/* A sparse matrix on the device.  CSR: ptr = row_ptr[nrows+1], idx = col_idx[nnz].
+ * CSC (the pull path's B^T, sparse.py:257-266): ptr = col_ptr[ncols+1],
+ * idx = row_idx[nnz].  Offsets are int64 like the reference (sparse.py:9);
+ * indices are int32 (all dimensions < 2^31).  values may be NULL for masks
+ * and for plus-pair operands (the reference never reads them, _kernels.py:56). */
+typedef struct {
+    int64_t nrows;
+    int64_t ncols;
+    int64_t nnz;
+    const int64_t* ptr;
+    const int32_t* idx;
+    const void* values;
+} mm_matrix_t;
+
+/* MultiplyPlan (multiply.py:46-81).  workers/grain have no GPU meaning. */
+typedef struct {
+    int32_t algorithm;     /* MM_ALGO_* */
+    int32_t phases;        /* 1 = one-phase (bounded + compact), 2 = symbolic + exact */
+    int32_t complemented;  /* plan.complemented OR mask.complemented (multiply.py:181) */
+    int32_t semiring;      /* MM_SR_* */
+    int32_t dtype;         /* MM_DTYPE_* */
+    int32_t n_inspect;     /* heap: -1 = inf, 0, 1 (multiply.py:227-228) */
+} mm_plan_t;
+
+/* MultiplyStats (multiply.py:84-100) */
+typedef struct {
+    int64_t generated_flops;      /* sum over A nonzeros of nnz(B_k*) */
+    int64_t evaluated_multiplies; /* products computed after mask filtering */
+    int64_t output_nnz;
+    int64_t rows_push;            /* rows computed by push kernels */
+    int64_t rows_pull;            /* rows computed by the pull (inner) kernel */
+    int64_t rows_empty;           /* rows skipped (empty mask row / zero flops) */
+} mm_stats_t;
+
+typedef struct mm_handle mm_handle_t;
+
+int mm_abi_version(void);
+const char* mm_last_error(void);
+
+/* One handle per device; owns the stream-ordered workspace pool and the
+ * state carried between mm_multiply_begin and mm_multiply_end. */
+int mm_create(int device, mm_handle_t** out);
+int mm_destroy(mm_handle_t* h);
+
+/*
+ * Two-call protocol for masked_multiply_with_stats (multiply.py:349-403):
+ *
+ *   mm_multiply_begin: validation (_Prepared, multiply.py:175-233), per-row
+ *     work estimate (flops_per_row, :103-108), row binning, then
+ *       1P: bounded numeric into workspace slots (:377-387) and the exact
+ *           row-pointer scan (:391-393);
+ *       2P: symbolic phase + exclusive scan (:358-368).
+ *     Writes nnz(C) to *out_nnz (one small device->host readback).
+ *   The caller allocates c_col_idx[nnz] (int32) and c_values[nnz] (dtype).
+ *   mm_multiply_end: 1P compaction (compact_rows, _kernels.py:586-594) or 2P
+ *     numeric into the exact slots (:369-376); copies row_ptr[nrows+1] and
+ *     fills *stats.  Returns MM_ERR_INTERNAL if the reference's assertions
+ *     (multiply.py:375,390) would fail.
+ *
+ * b: B as CSR (required: push kernels and flops_per_row read it).
+ * b_csc: B^T storage (CSC) for the pull path; required when
+ *   plan->algorithm is MM_ALGO_INNER, optional for MM_ALGO_AUTO (without it
+ *   AUTO runs push only), ignored otherwise.
+ * mask: pattern only (values ignored); complement via plan->complemented.
+ */
+int mm_multiply_begin(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask,
+                      const mm_matrix_t* a, const mm_matrix_t* b, const mm_matrix_t* b_csc,
+                      void* stream, int64_t* out_nnz);
+int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_values,
+                    mm_stats_t* stats);
+
+/* Per-phase device timing (CUDA events recorded on the caller's stream) of
+ * every later multiply on this handle; off by default.  mm_profile_read
+ * waits for the last multiply and returns ms[0..5] = {analyze + bin summary,
+ * bin scatter, numeric (1P) or symbolic (2P) kernels, row-pointer scan and
+ * nnz readback, compaction (1P) or numeric (2P), whole multiply} and the
+ * number of kernels the library launched for it. */
+int mm_profile_enable(mm_handle_t* h, int on);
+int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
+
+/* symbolic_phase (multiply.py:411-419): exact per-row output counts into the
+ * device array counts[mask->nrows] (int64).  Synchronous on `stream`. */
+int mm_symbolic(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask,
+                const mm_matrix_t* a, const mm_matrix_t* b, const mm_matrix_t* b_csc,
+                void* stream, int64_t* counts);
+
+/* ---- building blocks (stream-ordered, device pointers) ---- */
+
+/* flops_per_row (multiply.py:103-108): row_flops[i] = sum_{k in A_i} nnz(B_k*);
+ * *total (device int64) receives the sum (generated_flops, :353). */
+int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops, int64_t* total,
+                 void* stream);
+
+/* np.cumsum into a row pointer (multiply.py:366-367,391-392):
+ * out[0] = 0, out[i+1] = out[i] + counts[i]; n+1 outputs. */
+int mm_exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, void* stream);
+
+/* compact_rows (_kernels.py:586-594) with int32 indices. */
+int mm_compact_rows(int64_t nrows, const int64_t* bounds_off, const int64_t* row_nnz,
+                    const int32_t* tmp_idx, const void* tmp_val, const int64_t* out_ptr,
+                    int32_t* out_idx, void* out_val, int dtype, void* stream);
+
+/* sum of values[0..n) into *out (device, int64 or float64) — the triangle
+ * count reduction of triangle_count (graphs.py:96). */
+int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MASKMUL_B200_H */

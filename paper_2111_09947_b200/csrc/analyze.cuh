@@ -1,0 +1,215 @@
+// Row analysis, binning and row-list construction.
+//
+// Reference: flops_per_row (multiply.py:103-108), the per-row hash capacity
+// rule (multiply.py:220-226), one_phase_bounds (multiply.py:230-233) and the
+// empty-row short-circuits of every kernel (_kernels.py:42-44,143-145,284-286,
+// 441-443).  On the GPU the same per-row quantities decide which kernel tier
+// computes the row: a row's tier depends only on the row itself, so results
+// are independent of how rows are partitioned across launches or devices.
+#pragma once
+#include "common.cuh"
+
+namespace mm {
+
+// Kernel families (the paper's accumulators) + the pull path.
+enum Family : int { FAM_HASH = 0, FAM_MSA = 1, FAM_MCA = 2, FAM_HEAP = 3, FAM_PULL = 4, FAM_AUTO = 5 };
+
+// Hash-family modes.
+enum Mode : int { MODE_PLAIN = 0, MODE_CTAB = 1, MODE_CSRCH = 2 };
+
+// Bins.  0 = nothing to compute (row_nnz = 0).
+enum Bin : int {
+    BIN_EMPTY = 0,
+    BIN_HASH0 = 1,    // + mode*4 + tier   (tiers 0..3)
+    BIN_PULL = 13,
+    BIN_MSA = 14,
+    BIN_MCA = 15,
+    BIN_HEAP = 16,
+    NBINS = 17
+};
+
+__host__ __device__ constexpr int hash_bin(int mode, int tier) { return BIN_HASH0 + mode * 4 + tier; }
+
+// Hash tiers: group width (warps) and the largest table (log2 entries) each
+// tier keeps in shared memory.  Tier 3 keeps its table in global memory.
+__host__ __device__ constexpr int tier_gw(int t) { return t == 0 ? 1 : (t == 1 ? 4 : (t == 2 ? 16 : 32)); }
+__host__ __device__ constexpr int tier_cap_lg_pair(int t) { return t == 0 ? 10 : (t == 1 ? 13 : (t == 2 ? 14 : 30)); }
+__host__ __device__ constexpr int tier_cap_lg_val(int t) { return t == 0 ? 10 : (t == 1 ? 12 : (t == 2 ? 13 : 30)); }
+constexpr int64_t TIER_FLOPS0 = 4096;
+constexpr int64_t TIER_FLOPS1 = 65536;
+
+struct Summary {
+    unsigned long long gen_flops;
+    unsigned long long bound_total;
+    unsigned long long evaluated;
+    long long total_nnz;
+    int bin_count[NBINS];
+    int bin_cap_lg[NBINS];
+    int max_na;
+    int max_nm;
+    int flag;
+    int pad;
+};
+
+struct AnalyzeParams {
+    int family;      // Family
+    int comp;        // complemented mask
+    int ordered;     // fp64 plus-times: single-warp ordered accumulation
+    int pair;        // plus-pair (4-byte table values)
+    int vbytes;      // value bytes read per operand entry (0 plus-pair, 8 otherwise)
+    int has_bt;      // B^T (CSC) available
+};
+
+__device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
+    return pair ? tier_cap_lg_pair(tier) : tier_cap_lg_val(tier);
+}
+
+// Chooses the bin for a row and the table size (log2) the row will use.
+__device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na, int64_t nm,
+                                            int64_t flops, int64_t ncols, int64_t pull_cols,
+                                            int* cap_lg_out) {
+    *cap_lg_out = 0;
+    if (flops == 0 || (!ap.comp && nm == 0)) return BIN_EMPTY;
+    int fam = ap.family;
+    if (fam == FAM_AUTO) {
+        fam = FAM_HASH;
+        if (!ap.comp && ap.has_bt) {
+            // per-row byte cost model: push vs pull
+            int64_t w = 4 + ap.vbytes;
+            int64_t push = 16 * na + flops * w;
+            int64_t pull = 16 * nm + (nm * na + pull_cols) * w;
+            if (pull < push) fam = FAM_PULL;
+        }
+    }
+    if (fam == FAM_PULL) return BIN_PULL;
+    // MSA / MCA / heap families are routed through their own bins when the
+    // kernels exist; until then they share the hash tiers (same results).
+    int64_t fc = flops < ncols ? flops : ncols;
+    int mode;
+    int64_t keys;
+    if (!ap.comp) {
+        mode = MODE_PLAIN;
+        keys = nm;
+    } else {
+        int lgm = 1;
+        while ((1ll << lgm) <= nm) lgm++;
+        // membership by binary search when it is cheaper than marking the mask
+        if (fc * lgm <= nm) {
+            mode = MODE_CSRCH;
+            keys = fc;
+        } else {
+            mode = MODE_CTAB;
+            keys = nm + fc;
+        }
+    }
+    int need = ceil_log2_i64(2 * keys);
+    if (need < 5) need = 5;
+    int want = ceil_log2_i64(4 * keys);
+    if (want < 5) want = 5;
+    int tier;
+    if (ap.ordered) {
+        tier = need <= tier_cap_lg_val(0) ? 0 : 3;
+    } else {
+        int tc = 3;
+        for (int t = 0; t < 3; t++) {
+            if (need <= tier_cap_lg(ap.pair, t)) { tc = t; break; }
+        }
+        int tf = flops <= TIER_FLOPS0 ? 0 : (flops <= TIER_FLOPS1 ? 1 : 2);
+        tier = tc > tf ? tc : tf;
+    }
+    int lim = tier_cap_lg(ap.pair, tier);
+    *cap_lg_out = want < lim ? want : lim;
+    return hash_bin(mode, tier);
+}
+
+// One warp per row.  Computes row_flops, 1P complement bounds, bin + table size.
+__global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64_t* row_flops,
+                                                 int64_t* bound, uint8_t* row_bin, int8_t* row_cap_lg,
+                                                 Summary* s) {
+    __shared__ int s_count[NBINS];
+    __shared__ int s_cap[NBINS];
+    __shared__ unsigned long long s_flops, s_bound;
+    __shared__ int s_na, s_nm;
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) { s_count[b] = 0; s_cap[b] = 0; }
+    if (threadIdx.x == 0) { s_flops = 0; s_bound = 0; s_na = 0; s_nm = 0; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long my_flops = 0, my_bound = 0;
+    for (int64_t i = warp; i < p.nrows; i += nwarps) {
+        int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1];
+        long long f = 0;
+        for (int64_t t = as + lane; t < ae; t += 32) {
+            int32_t k = p.a_idx[t];
+            f += p.b_ptr[k + 1] - p.b_ptr[k];
+        }
+        f = warp_sum_ll(f);
+        int64_t ms = p.m_ptr[i], me = p.m_ptr[i + 1];
+        int64_t nm = me - ms;
+        long long pull_cols = 0;
+        if (ap.family == FAM_AUTO && ap.has_bt && !ap.comp && f > 0 && nm > 0) {
+            for (int64_t t = ms + lane; t < me; t += 32) {
+                int32_t j = p.m_idx[t];
+                pull_cols += p.bt_ptr[j + 1] - p.bt_ptr[j];
+            }
+            pull_cols = warp_sum_ll(pull_cols);
+        }
+        if (lane == 0) {
+            int64_t na = ae - as;
+            row_flops[i] = f;
+            if (bound) {
+                int64_t bd = f < p.ncols ? f : p.ncols;
+                bound[i] = bd;
+                my_bound += bd;
+            }
+            int cap_lg;
+            int b = classify_row(ap, na, nm, f, p.ncols, pull_cols, &cap_lg);
+            row_bin[i] = (uint8_t)b;
+            row_cap_lg[i] = (int8_t)cap_lg;
+            atomicAdd(&s_count[b], 1);
+            atomicMax(&s_cap[b], cap_lg);
+            atomicMax(&s_na, (int)(na < 0x7fffffff ? na : 0x7fffffff));
+            atomicMax(&s_nm, (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
+            my_flops += f;
+        }
+    }
+    if (lane == 0) {
+        atomicAdd(&s_flops, my_flops);
+        atomicAdd(&s_bound, my_bound);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) {
+        if (s_count[b]) {
+            atomicAdd(&s->bin_count[b], s_count[b]);
+            atomicMax(&s->bin_cap_lg[b], s_cap[b]);
+        }
+    }
+    if (threadIdx.x == 0) {
+        atomicAdd(&s->gen_flops, s_flops);
+        atomicAdd(&s->bound_total, s_bound);
+        atomicMax(&s->max_na, s_na);
+        atomicMax(&s->max_nm, s_nm);
+    }
+}
+
+// Scatter row ids into per-bin lists (warp-aggregated atomics).
+__global__ void __launch_bounds__(256) k_bin_scatter(int64_t nrows, const uint8_t* row_bin,
+                                                     const int32_t* bin_off, int32_t* bin_cursor,
+                                                     int32_t* rows_out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nrows;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        int b = i < nrows ? row_bin[i] : 0;
+        unsigned peers = __match_any_sync(FULL, b);
+        int leader = __ffs(peers) - 1;
+        int rank = __popc(peers & lanemask_lt());
+        int start = 0;
+        if (lane == leader && b != 0) start = atomicAdd(&bin_cursor[b], __popc(peers));
+        start = __shfl_sync(FULL, start, leader);
+        if (b != 0) rows_out[bin_off[b] + start + rank] = (int32_t)i;
+    }
+}
+
+}  // namespace mm

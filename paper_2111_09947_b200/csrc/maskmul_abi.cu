@@ -1,0 +1,661 @@
+// C ABI of the B200 masked SpGEMM (declared in include/maskmul_b200.h).
+//
+// Host orchestration of one multiply, replacing the body of the reference's
+// masked_multiply_with_stats (pkg/src/maskmul/multiply.py:349-403):
+//   validate (_Prepared :175-233) -> k_analyze (flops_per_row, bins, bounds)
+//   -> one summary readback -> k_bin_scatter -> per-bin kernels
+//   -> scan -> nnz readback | compaction (1P) or exact numeric (2P).
+// Workspace comes from the device's stream-ordered memory pool
+// (cudaMallocAsync), so repeated multiplies allocate nothing from the OS.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/maskmul_b200.h"
+#include "analyze.cuh"
+#include "common.cuh"
+#include "pull_inner.cuh"
+#include "push_hash.cuh"
+#include "scan_compact.cuh"
+
+using namespace mm;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local long long g_launches = 0;   // kernels launched by this thread (profiling)
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return fail(MM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+}  // namespace
+
+struct mm_handle {
+    int device = 0;
+    int num_sms = 148;
+    Summary* h_summary = nullptr;   // pinned
+    long long* h_scalar = nullptr;  // pinned
+    // ---- state between begin and end ----
+    bool active = false;
+    cudaStream_t stream = nullptr;
+    mm_plan_t plan{};
+    Prob prob{};
+    AnalyzeParams ap{};
+    int kind = 0;        // 0 plus-pair, 1 int64 plus-times, 2 float64 plus-times (ordered)
+    int out_f64 = 0;
+    int64_t nrows = 0, ncols = 0;
+    std::vector<void*> allocs;
+    Summary* d_summary = nullptr;
+    int64_t* row_flops = nullptr;
+    int64_t* bound = nullptr;
+    int64_t* bound_ptr = nullptr;      // 1P complement bound offsets (nrows+1)
+    const int64_t* bound_off = nullptr;
+    uint8_t* row_bin = nullptr;
+    int8_t* row_cap_lg = nullptr;
+    int32_t* rows_list = nullptr;
+    int32_t* cursors = nullptr;        // 2 * NBINS fetch counters
+    int32_t* d_bin_off = nullptr;
+    int64_t* row_nnz = nullptr;
+    int64_t* row_nnz2 = nullptr;
+    int64_t* c_row_ptr = nullptr;
+    int32_t* tmp_idx = nullptr;
+    void* tmp_val = nullptr;
+    int64_t total_nnz = 0;
+    int bin_off[NBINS + 1] = {0};
+    Summary sum{};
+    mm_stats_t stats{};
+    // ---- profiling ----
+    bool prof = false;
+    cudaEvent_t ev[6] = {};
+    long long launch_base = 0, launches = 0;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(mm_handle* h, T** p, size_t count) {
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    void* q = nullptr;
+    CU(cudaMallocAsync(&q, bytes, h->stream));
+    h->allocs.push_back(q);
+    *p = (T*)q;
+    return MM_OK;
+}
+
+void release(mm_handle* h) {
+    for (void* q : h->allocs) cudaFreeAsync(q, h->stream);
+    h->allocs.clear();
+    h->active = false;
+}
+
+// ---- scan ----
+int scan_impl(const int64_t* in, int64_t n, int64_t* out_incl, cudaStream_t st,
+              std::vector<void*>& tmp) {
+    // out_incl[0..n) = inclusive scan of in
+    if (n <= 0) return MM_OK;
+    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    int64_t* partials = nullptr;
+    CU(cudaMallocAsync((void**)&partials, (nb + 1) * sizeof(int64_t), st));
+    tmp.push_back(partials);
+    ++g_launches;
+    k_scan_tile<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, out_incl, partials);
+    if (nb > 1) {
+        int64_t* pscan = nullptr;
+        CU(cudaMallocAsync((void**)&pscan, (nb + 1) * sizeof(int64_t), st));
+        tmp.push_back(pscan);
+        // exclusive offsets per tile: pscan[0] = 0, pscan[1..nb] = incl(partials)
+        ++g_launches;
+        k_set_zero_i64<<<1, 1, 0, st>>>(pscan);
+        int rc = scan_impl(partials, nb, pscan + 1, st, tmp);
+        if (rc) return rc;
+        ++g_launches;
+        k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out_incl, n, pscan);
+    }
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+int exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, cudaStream_t st) {
+    std::vector<void*> tmp;
+    ++g_launches;
+    k_set_zero_i64<<<1, 1, 0, st>>>(out);
+    int rc = scan_impl(counts, n, out + 1, st, tmp);
+    for (void* q : tmp) cudaFreeAsync(q, st);
+    CU(cudaGetLastError());
+    return rc;
+}
+
+int validate(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+             const mm_matrix_t* b, const mm_matrix_t* bt) {
+    if (!plan || !mask || !a || !b) return fail(MM_ERR_INPUT, "null argument");
+    if (plan->algorithm < MM_ALGO_MSA || plan->algorithm > MM_ALGO_AUTO)
+        return fail(MM_ERR_PLAN, "unknown algorithm");
+    if (plan->phases != 1 && plan->phases != 2) return fail(MM_ERR_PLAN, "phases must be 1 or 2");
+    if (plan->semiring != MM_SR_ARITHMETIC && plan->semiring != MM_SR_PLUS_PAIR)
+        return fail(MM_ERR_PLAN, "unknown semiring");
+    if (plan->dtype != MM_DTYPE_INT64 && plan->dtype != MM_DTYPE_FLOAT64)
+        return fail(MM_ERR_PLAN, "dtype must be int64 or float64");
+    if (plan->n_inspect < -1 || plan->n_inspect > 1) return fail(MM_ERR_PLAN, "n_inspect must be 0, 1 or inf");
+    if (plan->complemented && plan->algorithm == MM_ALGO_MCA)
+        return fail(MM_ERR_PLAN, "the mask-compressed accumulator does not support complemented masks");
+    if (plan->complemented && plan->algorithm == MM_ALGO_INNER)
+        return fail(MM_ERR_PLAN, "the inner-product algorithm does not support complemented masks");
+    if (mask->nrows != a->nrows || mask->ncols != b->ncols || a->ncols != b->nrows)
+        return fail(MM_ERR_INPUT, "dimension mismatch: mask (" + std::to_string(mask->nrows) + ", " +
+                                      std::to_string(mask->ncols) + "), A (" + std::to_string(a->nrows) +
+                                      ", " + std::to_string(a->ncols) + "), B (" +
+                                      std::to_string(b->nrows) + ", " + std::to_string(b->ncols) + ")");
+    if (a->nrows < 0 || a->nrows >= (1ll << 31) || b->ncols >= (1ll << 31) || a->ncols >= (1ll << 31))
+        return fail(MM_ERR_INPUT, "dimensions must be < 2^31");
+    if ((a->nnz && (!a->ptr || !a->idx)) || !a->ptr || !b->ptr || !mask->ptr)
+        return fail(MM_ERR_INPUT, "missing index arrays");
+    if (plan->semiring == MM_SR_ARITHMETIC && ((a->nnz && !a->values) || (b->nnz && !b->values)))
+        return fail(MM_ERR_INPUT, "plus-times needs operand values");
+    if (plan->algorithm == MM_ALGO_INNER) {
+        if (!bt || !bt->ptr) return fail(MM_ERR_INPUT, "the inner-product algorithm needs B in CSC form");
+        if (bt->nrows != b->nrows || bt->ncols != b->ncols)
+            return fail(MM_ERR_INPUT, "B^T (CSC) shape differs from B");
+        if (plan->semiring == MM_SR_ARITHMETIC && bt->nnz && !bt->values)
+            return fail(MM_ERR_INPUT, "plus-times needs B^T values");
+    }
+    return MM_OK;
+}
+
+typedef void (*HashKernel)(Prob, Out, Work, const int8_t*, int, unsigned char*);
+
+template <int KIND, int MODE, bool NUM>
+HashKernel pick_hash_unordered(int tier, int* gw) {
+    switch (tier) {
+        case 0: *gw = 1; return k_push_hash<1, true, KIND, MODE, NUM>;
+        case 1: *gw = 4; return k_push_hash<4, true, KIND, MODE, NUM>;
+        case 2: *gw = 16; return k_push_hash<16, true, KIND, MODE, NUM>;
+        default: *gw = 32; return k_push_hash<32, false, KIND, MODE, NUM>;
+    }
+}
+
+template <int MODE>
+HashKernel pick_hash_ordered(int tier, int* gw) {
+    *gw = 1;
+    return tier == 0 ? k_push_hash<1, true, 2, MODE, true> : k_push_hash<1, false, 2, MODE, true>;
+}
+
+template <int MODE>
+HashKernel pick_hash_mode(int kind, int tier, bool numeric, int* gw) {
+    if (!numeric) return pick_hash_unordered<0, MODE, false>(tier, gw);
+    if (kind == 0) return pick_hash_unordered<0, MODE, true>(tier, gw);
+    if (kind == 1) return pick_hash_unordered<1, MODE, true>(tier, gw);
+    return pick_hash_ordered<MODE>(tier, gw);
+}
+
+HashKernel pick_hash(int kind, int mode, int tier, bool numeric, int* gw) {
+    if (mode == MODE_PLAIN) return pick_hash_mode<MODE_PLAIN>(kind, tier, numeric, gw);
+    if (mode == MODE_CTAB) return pick_hash_mode<MODE_CTAB>(kind, tier, numeric, gw);
+    return pick_hash_mode<MODE_CSRCH>(kind, tier, numeric, gw);
+}
+
+// Launch every non-empty bin.  numeric=false: symbolic counts into out.row_nnz.
+int launch_bins(mm_handle* h, bool numeric, const Out& out) {
+    cudaStream_t st = h->stream;
+    int32_t* cursors = h->cursors + (numeric ? NBINS : 0);
+    for (int b = 1; b < NBINS; b++) {
+        int cnt = h->sum.bin_count[b];
+        if (!cnt) continue;
+        Work wk{h->rows_list + h->bin_off[b], cnt, cursors + b};
+        if (b == BIN_PULL) {
+            int kind = numeric ? h->kind : 0;
+            int stage = std::min(std::max(h->sum.max_na, 2), 512);
+            stage += stage & 1;
+            size_t esz = kind == 0 ? 4 : 12;
+            size_t smem = (size_t)8 * stage * esz;
+            void (*kern)(Prob, Out, Work, int);
+            if (!numeric) kern = k_pull_inner<0, false>;
+            else if (kind == 0) kern = k_pull_inner<0, true>;
+            else if (kind == 1) kern = k_pull_inner<1, true>;
+            else kern = k_pull_inner<2, true>;
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            int grid = std::max(1, std::min((cnt + 7) / 8, std::max(occ, 1) * h->num_sms));
+            ++g_launches;
+            kern<<<grid, 256, smem, st>>>(h->prob, out, wk, stage);
+            CU(cudaGetLastError());
+            continue;
+        }
+        if (b >= BIN_HASH0 && b < BIN_HASH0 + 12) {
+            int mode = (b - BIN_HASH0) / 4, tier = (b - BIN_HASH0) % 4;
+            int kind = numeric ? h->kind : 0;
+            int gw = 1;
+            HashKernel kern = pick_hash(kind, mode, tier, numeric, &gw);
+            bool smem_table = kind == 2 ? tier == 0 : tier < 3;
+            int threads = gw == 32 ? 1024 : (gw == 16 ? 512 : 256);
+            int groups = threads / (32 * gw);
+            int cap_lg = std::max(h->sum.bin_cap_lg[b], 5);
+            size_t ebytes = kind == 0 ? 8 : 16;
+            size_t table = ((size_t)1 << cap_lg) * ebytes;
+            size_t smem = smem_table ? groups * table : 0;
+            if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "hash tier table exceeds shared memory");
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
+            unsigned char* gslab = nullptr;
+            if (!smem_table) {
+                size_t bytes = (size_t)grid * groups * table;
+                CU(cudaMallocAsync((void**)&gslab, bytes, st));
+                h->allocs.push_back(gslab);
+            }
+            ++g_launches;
+            kern<<<grid, threads, smem, st>>>(h->prob, out, wk, h->row_cap_lg, cap_lg, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
+        return fail(MM_ERR_INTERNAL, "unhandled bin " + std::to_string(b));
+    }
+    return MM_OK;
+}
+
+void mark(mm_handle* h, int k) {
+    if (h->prof) cudaEventRecord(h->ev[k], h->stream);
+}
+
+int sync_read(mm_handle* h, void* dst, const void* src, size_t bytes) {
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return MM_OK;
+}
+
+int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+               const mm_matrix_t* b, const mm_matrix_t* bt, cudaStream_t st, bool symbolic_only,
+               int64_t* counts_out, int64_t* out_nnz) {
+    int rc = validate(plan, mask, a, b, bt);
+    if (rc) return rc;
+    if (h->active) release(h);
+    CU(cudaSetDevice(h->device));
+    h->stream = st;
+    h->launch_base = g_launches;
+    mark(h, 0);
+    h->plan = *plan;
+    h->nrows = mask->nrows;
+    h->ncols = mask->ncols;
+    const bool comp = plan->complemented != 0;
+    const bool pair = plan->semiring == MM_SR_PLUS_PAIR;
+    h->kind = pair ? 0 : (plan->dtype == MM_DTYPE_FLOAT64 ? 2 : 1);
+    h->out_f64 = plan->dtype == MM_DTYPE_FLOAT64;
+    Prob& p = h->prob;
+    p.a_ptr = a->ptr; p.a_idx = a->idx; p.a_val = a->values;
+    p.b_ptr = b->ptr; p.b_idx = b->idx; p.b_val = b->values;
+    p.m_ptr = mask->ptr; p.m_idx = mask->idx;
+    const bool use_bt = bt && bt->ptr && (plan->algorithm == MM_ALGO_INNER || plan->algorithm == MM_ALGO_AUTO);
+    p.bt_ptr = use_bt ? bt->ptr : nullptr;
+    p.bt_idx = use_bt ? bt->idx : nullptr;
+    p.bt_val = use_bt ? bt->values : nullptr;
+    p.nrows = h->nrows;
+    p.ncols = h->ncols;
+    AnalyzeParams& ap = h->ap;
+    switch (plan->algorithm) {
+        case MM_ALGO_INNER: ap.family = FAM_PULL; break;
+        case MM_ALGO_AUTO: ap.family = FAM_AUTO; break;
+        default: ap.family = FAM_HASH; break;   // msa/mca/heap: see classify_row
+    }
+    ap.comp = comp;
+    ap.ordered = h->kind == 2;
+    ap.pair = pair;
+    ap.vbytes = pair ? 0 : 8;
+    ap.has_bt = use_bt;
+    const int64_t m = h->nrows;
+
+    if ((rc = dalloc(h, &h->d_summary, 1))) return rc;
+    if ((rc = dalloc(h, &h->row_flops, m))) return rc;
+    p.row_flops = h->row_flops;
+    if ((rc = dalloc(h, &h->row_bin, m))) return rc;
+    if ((rc = dalloc(h, &h->row_cap_lg, m))) return rc;
+    if ((rc = dalloc(h, &h->rows_list, m))) return rc;
+    if ((rc = dalloc(h, &h->cursors, 2 * NBINS))) return rc;
+    if ((rc = dalloc(h, &h->d_bin_off, NBINS + 1))) return rc;
+    if ((rc = dalloc(h, &h->row_nnz, m))) return rc;
+    if ((rc = dalloc(h, &h->c_row_ptr, m + 1))) return rc;
+    const bool need_bound = comp && plan->phases == 1 && !symbolic_only;
+    if (need_bound) {
+        if ((rc = dalloc(h, &h->bound, m))) return rc;
+        if ((rc = dalloc(h, &h->bound_ptr, m + 1))) return rc;
+    } else {
+        h->bound = nullptr;
+        h->bound_ptr = nullptr;
+    }
+    CU(cudaMemsetAsync(h->d_summary, 0, sizeof(Summary), st));
+    CU(cudaMemsetAsync(h->cursors, 0, 2 * NBINS * sizeof(int32_t), st));
+    if (m > 0) CU(cudaMemsetAsync(h->row_nnz, 0, m * sizeof(int64_t), st));
+
+    if (m > 0) {
+        int grid = (int)std::min<int64_t>((m + 7) / 8, (int64_t)h->num_sms * 16);
+        ++g_launches;
+        k_analyze<<<grid, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin, h->row_cap_lg,
+                                        h->d_summary);
+        CU(cudaGetLastError());
+    }
+    if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+    h->sum = *h->h_summary;
+    mark(h, 1);
+    h->bin_off[0] = 0;
+    for (int b = 0; b < NBINS; b++) h->bin_off[b + 1] = h->bin_off[b] + (b == 0 ? 0 : h->sum.bin_count[b]);
+    h->stats = mm_stats_t{};
+    h->stats.generated_flops = (int64_t)h->sum.gen_flops;
+    h->stats.rows_empty = h->sum.bin_count[BIN_EMPTY];
+    h->stats.rows_pull = h->sum.bin_count[BIN_PULL];
+    h->stats.rows_push = m - h->stats.rows_empty - h->stats.rows_pull;
+    if (m > 0) {
+        CU(cudaMemcpyAsync(h->d_bin_off, h->bin_off, (NBINS + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        // the pinned copy of bin_off must stay alive until the copy runs: bin_off
+        // lives in the handle, which outlives the stream work
+        int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8);
+        ++g_launches;
+        k_bin_scatter<<<grid, 256, 0, st>>>(m, h->row_bin, h->d_bin_off, h->cursors, h->rows_list);
+        CU(cudaGetLastError());
+        CU(cudaMemsetAsync(h->cursors, 0, 2 * NBINS * sizeof(int32_t), st));
+    }
+    mark(h, 2);
+
+    if (symbolic_only || plan->phases == 2) {
+        Out o{};
+        o.row_nnz = symbolic_only ? counts_out : h->row_nnz;
+        if ((rc = launch_bins(h, false, o))) return rc;
+        mark(h, 3);
+        if (symbolic_only) {
+            CU(cudaStreamSynchronize(st));
+            return MM_OK;
+        }
+        if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st))) return rc;
+        if ((rc = sync_read(h, h->h_scalar, h->c_row_ptr + m, sizeof(long long)))) return rc;
+        h->total_nnz = *h->h_scalar;
+        mark(h, 4);
+        *out_nnz = h->total_nnz;
+        h->active = true;
+        return MM_OK;
+    }
+
+    // ---- one-phase: bounded numeric into slots, then exact row pointer ----
+    int64_t tmp_total;
+    if (comp) {
+        if ((rc = exclusive_scan(h->bound, m, h->bound_ptr, st))) return rc;
+        h->bound_off = h->bound_ptr;
+        tmp_total = (int64_t)h->sum.bound_total;
+    } else {
+        h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
+        tmp_total = mask->nnz;
+    }
+    if ((rc = dalloc(h, &h->tmp_idx, tmp_total))) return rc;
+    void* tv = nullptr;
+    CU(cudaMallocAsync(&tv, std::max<size_t>(tmp_total * 8, 16), st));
+    h->allocs.push_back(tv);
+    h->tmp_val = tv;
+    Out o{};
+    o.off = h->bound_off;
+    o.idx = h->tmp_idx;
+    o.val = h->tmp_val;
+    o.row_nnz = h->row_nnz;
+    o.evaluated = &h->d_summary->evaluated;
+    o.out_f64 = h->out_f64;
+    if ((rc = launch_bins(h, true, o))) return rc;
+    mark(h, 3);
+    if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st))) return rc;
+    CU(cudaMemcpyAsync(&h->d_summary->total_nnz, h->c_row_ptr + m, sizeof(long long),
+                       cudaMemcpyDeviceToDevice, st));
+    if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+    h->total_nnz = h->h_summary->total_nnz;
+    h->stats.evaluated_multiplies = (int64_t)h->h_summary->evaluated;
+    mark(h, 4);
+    *out_nnz = h->total_nnz;
+    h->active = true;
+    return MM_OK;
+}
+
+int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_values, mm_stats_t* stats) {
+    if (!h->active) return fail(MM_ERR_INPUT, "mm_multiply_end without a successful mm_multiply_begin");
+    cudaStream_t st = h->stream;
+    const int64_t m = h->nrows;
+    int rc;
+    if (h->total_nnz > 0 && (!c_col_idx || !c_values))
+        return fail(MM_ERR_INPUT, "output arrays required for a non-empty result");
+    if (c_row_ptr && c_row_ptr != h->c_row_ptr)
+        CU(cudaMemcpyAsync(c_row_ptr, h->c_row_ptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    int* flag = &h->d_summary->flag;
+    if (h->plan.phases == 1) {
+        if (m > 0) {
+            int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 16);
+            ++g_launches;
+            if (h->out_f64)
+                k_compact<double><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
+                                                        (const double*)h->tmp_val, h->c_row_ptr,
+                                                        c_col_idx, (double*)c_values, flag);
+            else
+        k_compact<long long><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
+                                                           (const long long*)h->tmp_val, h->c_row_ptr,
+                                                           c_col_idx, (long long*)c_values, flag);
+            CU(cudaGetLastError());
+        }
+        mark(h, 5);
+        // the bound flag is checked lazily: read it with the stats below
+        if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) { release(h); return rc; }
+    } else {
+        if ((rc = dalloc(h, &h->row_nnz2, m))) { release(h); return rc; }
+        if (m > 0) CU(cudaMemsetAsync(h->row_nnz2, 0, m * sizeof(int64_t), st));
+        Out o{};
+        o.off = h->c_row_ptr;
+        o.idx = c_col_idx;
+        o.val = c_values;
+        o.row_nnz = h->row_nnz2;
+        o.evaluated = &h->d_summary->evaluated;
+        o.out_f64 = h->out_f64;
+        if ((rc = launch_bins(h, true, o))) { release(h); return rc; }
+        if (m > 0) {
+            int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8);
+            ++g_launches;
+            k_check_equal<<<grid, 256, 0, st>>>(m, h->row_nnz, h->row_nnz2, flag);
+        }
+        mark(h, 5);
+        if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) { release(h); return rc; }
+        h->stats.evaluated_multiplies = (int64_t)h->h_summary->evaluated;
+    }
+    int bad = h->h_summary->flag;
+    h->launches = g_launches - h->launch_base;
+    h->stats.output_nnz = h->total_nnz;
+    if (stats) *stats = h->stats;
+    release(h);
+    if (bad)
+        return fail(MM_ERR_INTERNAL, h->plan.phases == 1 ? "one-phase row bound violated"
+                                                         : "symbolic phase disagreed with numeric row sizes");
+    return MM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mm_abi_version(void) { return MM_ABI_VERSION; }
+
+const char* mm_last_error(void) { return g_last_error.c_str(); }
+
+int mm_create(int device, mm_handle_t** out) {
+    if (!out) return fail(MM_ERR_INPUT, "null handle pointer");
+    mm_handle* h = new mm_handle();
+    h->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) { delete h; return fail(MM_ERR_CUDA, cudaGetErrorString(e)); }
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    if (cudaMallocHost((void**)&h->h_summary, sizeof(Summary)) != cudaSuccess ||
+        cudaMallocHost((void**)&h->h_scalar, sizeof(long long)) != cudaSuccess) {
+        delete h;
+        return fail(MM_ERR_CUDA, "cudaMallocHost failed");
+    }
+    *out = h;
+    return MM_OK;
+}
+
+int mm_destroy(mm_handle_t* h) {
+    if (!h) return MM_OK;
+    if (h->active) release(h);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    cudaFreeHost(h->h_summary);
+    cudaFreeHost(h->h_scalar);
+    for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    delete h;
+    return MM_OK;
+}
+
+int mm_multiply_begin(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+                      const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* out_nnz) {
+    if (!h || !out_nnz) return fail(MM_ERR_INPUT, "null argument");
+    int rc = begin_impl(h, plan, mask, a, b, b_csc, (cudaStream_t)stream, false, nullptr, out_nnz);
+    if (rc) release(h);
+    return rc;
+}
+
+int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_values, mm_stats_t* stats) {
+    if (!h) return fail(MM_ERR_INPUT, "null handle");
+    return end_impl(h, c_row_ptr, c_col_idx, c_values, stats);
+}
+
+int mm_profile_enable(mm_handle_t* h, int on) {
+    if (!h) return fail(MM_ERR_INPUT, "null handle");
+    if (on && !h->ev[0]) {
+        for (auto& e : h->ev) CU(cudaEventCreate(&e));
+    }
+    h->prof = on != 0;
+    return MM_OK;
+}
+
+int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches) {
+    if (!h) return fail(MM_ERR_INPUT, "null handle");
+    if (launches) *launches = h->launches;
+    if (!h->prof || !ms) return MM_OK;
+    CU(cudaEventSynchronize(h->ev[5]));
+    static const int from[6] = {0, 1, 2, 3, 4, 0};
+    static const int to[6] = {1, 2, 3, 4, 5, 5};
+    for (int q = 0; q < n && q < 6; q++) {
+        float t = 0.f;
+        CU(cudaEventElapsedTime(&t, h->ev[from[q]], h->ev[to[q]]));
+        ms[q] = t;
+    }
+    return MM_OK;
+}
+
+int mm_symbolic(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+                const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* counts) {
+    if (!h || !counts) return fail(MM_ERR_INPUT, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (mask && mask->nrows > 0) {
+        cudaError_t e = cudaMemsetAsync(counts, 0, mask->nrows * sizeof(int64_t), st);
+        if (e != cudaSuccess) return fail(MM_ERR_CUDA, cudaGetErrorString(e));
+    }
+    int64_t dummy = 0;
+    int rc = begin_impl(h, plan, mask, a, b, b_csc, st, true, counts, &dummy);
+    release(h);
+    if (!rc) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(MM_ERR_CUDA, cudaGetErrorString(e));
+    }
+    return rc;
+}
+
+int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops, int64_t* total, void* stream) {
+    if (!a || !b || !row_flops) return fail(MM_ERR_INPUT, "null argument");
+    if (a->ncols != b->nrows) return fail(MM_ERR_INPUT, "dimension mismatch");
+    cudaStream_t st = (cudaStream_t)stream;
+    Prob p{};
+    p.a_ptr = a->ptr; p.a_idx = a->idx; p.b_ptr = b->ptr; p.b_idx = b->idx;
+    // reuse the analysis kernel with a dummy all-rows mask view: only flops matter
+    p.m_ptr = a->ptr; p.m_idx = a->idx;
+    p.nrows = a->nrows; p.ncols = b->ncols;
+    AnalyzeParams ap{};
+    ap.family = FAM_HASH;
+    Summary* s = nullptr;
+    uint8_t* rb = nullptr;
+    int8_t* rc_lg = nullptr;
+    CU(cudaMallocAsync((void**)&s, sizeof(Summary), st));
+    CU(cudaMallocAsync((void**)&rb, std::max<int64_t>(a->nrows, 1), st));
+    CU(cudaMallocAsync((void**)&rc_lg, std::max<int64_t>(a->nrows, 1), st));
+    CU(cudaMemsetAsync(s, 0, sizeof(Summary), st));
+    if (a->nrows > 0) {
+        int grid = (int)std::min<int64_t>((a->nrows + 7) / 8, 148 * 16);
+        ++g_launches;
+        k_analyze<<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s);
+    }
+    if (total) CU(cudaMemcpyAsync(total, &s->gen_flops, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    cudaFreeAsync(s, st);
+    cudaFreeAsync(rb, st);
+    cudaFreeAsync(rc_lg, st);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+int mm_exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, void* stream) {
+    if (!out || (n > 0 && !counts)) return fail(MM_ERR_INPUT, "null argument");
+    return exclusive_scan(counts, n, out, (cudaStream_t)stream);
+}
+
+int mm_compact_rows(int64_t nrows, const int64_t* bounds_off, const int64_t* row_nnz, const int32_t* tmp_idx,
+                    const void* tmp_val, const int64_t* out_ptr, int32_t* out_idx, void* out_val, int dtype,
+                    void* stream) {
+    if (nrows <= 0) return MM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int* flag = nullptr;
+    CU(cudaMallocAsync((void**)&flag, sizeof(int), st));
+    CU(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    int grid = (int)std::min<int64_t>((nrows + 255) / 256, 148 * 16);
+    ++g_launches;
+    if (dtype == MM_DTYPE_FLOAT64)
+        k_compact<double><<<grid, 256, 0, st>>>(nrows, bounds_off, row_nnz, tmp_idx, (const double*)tmp_val,
+                                                out_ptr, out_idx, (double*)out_val, flag);
+    else
+        k_compact<long long><<<grid, 256, 0, st>>>(nrows, bounds_off, row_nnz, tmp_idx,
+                                                   (const long long*)tmp_val, out_ptr, out_idx,
+                                                   (long long*)out_val, flag);
+    int hflag = 0;
+    CU(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFreeAsync(flag, st);
+    if (hflag) return fail(MM_ERR_INTERNAL, "one-phase row bound violated");
+    return MM_OK;
+}
+
+int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* stream) {
+    if (!out) return fail(MM_ERR_INPUT, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nparts = 592;
+    void* partials = nullptr;
+    CU(cudaMallocAsync(&partials, nparts * 8, st));
+    if (dtype == MM_DTYPE_FLOAT64) {
+        ++g_launches;
+        k_reduce_partial<double><<<nparts, 256, 0, st>>>((const double*)values, n, (double*)partials);
+        ++g_launches;
+        k_reduce_final<double><<<1, 32, 0, st>>>((const double*)partials, nparts, (double*)out);
+    } else {
+        ++g_launches;
+        k_reduce_partial<long long><<<nparts, 256, 0, st>>>((const long long*)values, n, (long long*)partials);
+        ++g_launches;
+        k_reduce_final<long long><<<1, 32, 0, st>>>((const long long*)partials, nparts, (long long*)out);
+    }
+    cudaFreeAsync(partials, st);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,390 @@
+// Push path, hash accumulator: row-wise Gustavson with a table keyed on the
+// mask row.
+//
+// Reference semantics: hash_numeric / hash_symbolic (_kernels.py:130-268) —
+// per-row open addressing with linear probing, mask keys marked first
+// (:156-162), products probed (:169-171), absent keys discarded (plain,
+// :173-174) or claimed (complement, :175-180), complement output sorted
+// (:198), plain output in mask order (:208-216).  Every product that survives
+// the mask is counted in `evaluated` (the lazy-thunk rule).
+//
+// GPU form: a group of GW warps owns one row at a time and a table of
+// 2^cap_lg (key:int32, cnt:int32[, val:8B]) entries in shared memory
+// (tiers 0-2) or in a per-group global slab (tier 3).  The row's products are
+// enumerated as a flattened (k, s) space per batch of 32 A entries, so every
+// lane does useful work regardless of B row lengths; probes are smem atomics.
+//
+// KIND: 0 = plus-pair (cnt is the value), 1 = int64 plus-times (atomic add,
+// order-free and exact), 2 = float64 plus-times (single warp, products folded
+// in ascending k exactly like the reference: bit-identical to MSA/Hash/MCA).
+// MODE: MODE_PLAIN, MODE_CTAB (complement, mask marked in the table),
+// MODE_CSRCH (complement, mask membership by binary search).
+#pragma once
+#include "analyze.cuh"
+#include "common.cuh"
+
+namespace mm {
+
+template <int KIND>
+struct HashEntry {
+    static constexpr int bytes = KIND == 0 ? 8 : 16;
+};
+
+// Pointers into one group's table region.
+template <int KIND>
+struct Table {
+    int32_t* keys;
+    int32_t* cnt;
+    unsigned long long* val;   // KIND != 0: 8-byte payload (int64 bits or double bits)
+    __device__ __forceinline__ void bind(unsigned char* base, int cap_max) {
+        if (KIND == 0) {
+            keys = (int32_t*)base;
+            cnt = keys + cap_max;
+            val = nullptr;
+        } else {
+            val = (unsigned long long*)base;
+            keys = (int32_t*)(val + cap_max);
+            cnt = keys + cap_max;
+        }
+    }
+};
+
+// Find the slot of key j (present or absent).  Returns slot index whose key is
+// j, or the EMPTY slot where the probe sequence ended (negated - 1).
+__device__ __forceinline__ int probe_find(const int32_t* keys, int32_t j, int lg, uint32_t mask) {
+    uint32_t h = fib_hash(j, lg);
+    for (;;) {
+        int32_t k = keys[h];
+        if (k == j) return (int)h;
+        if (k == EMPTY_KEY) return -(int)h - 1;
+        h = (h + 1) & mask;
+    }
+}
+
+// Find-or-insert (complement modes).  Returns the slot holding j.
+__device__ __forceinline__ int probe_insert(int32_t* keys, int32_t j, int lg, uint32_t mask) {
+    uint32_t h = fib_hash(j, lg);
+    for (;;) {
+        int32_t k = keys[h];
+        if (k == j) return (int)h;
+        if (k == EMPTY_KEY) {
+            int32_t old = atomicCAS(&keys[h], EMPTY_KEY, j);
+            if (old == EMPTY_KEY || old == j) return (int)h;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+// Group-wide exclusive prefix count of `flag`; returns the prefix, writes the
+// group total to *total.  Uses s_warp[GW] scratch for GW > 1.
+template <int GW>
+__device__ __forceinline__ int group_prefix(bool flag, int* total, int* s_warp, int bar_id,
+                                            int gt) {
+    unsigned bal = __ballot_sync(FULL, flag);
+    int lane = gt & 31;
+    int in_warp = __popc(bal & lanemask_lt());
+    if (GW == 1) {
+        *total = __popc(bal);
+        return in_warp;
+    } else {
+        int w = gt >> 5;
+        if (lane == 0) s_warp[w] = __popc(bal);
+        group_bar(bar_id, GW * 32);
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < GW; q++) {
+            int c = s_warp[q];
+            if (q < w) before += c;
+            tot += c;
+        }
+        group_bar(bar_id, GW * 32);
+        *total = tot;
+        return before + in_warp;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T load_val(const void* p, int64_t i) {
+    return ((const T*)p)[i];
+}
+
+// ---------------------------------------------------------------------------
+// The row processor.
+// ---------------------------------------------------------------------------
+template <int GW, int KIND, int MODE, bool NUMERIC>
+__device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, int64_t i,
+                                         int cap_lg, int gt, int bar_id, int* s_warp,
+                                         unsigned long long& evaluated) {
+    constexpr int GT = GW * 32;
+    const int lane = gt & 31;
+    const int wg = gt >> 5;
+    const int cap = 1 << cap_lg;
+    const uint32_t cmask = (uint32_t)cap - 1;
+    const int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1];
+    const int64_t ms = p.m_ptr[i], me = p.m_ptr[i + 1];
+
+    // 1. clear the table
+    for (int e = gt; e < cap; e += GT) {
+        tb.keys[e] = EMPTY_KEY;
+        tb.cnt[e] = 0;
+        if (KIND == 1) tb.val[e] = 0ull;
+    }
+    group_bar(bar_id, GT);
+    // 2. mark the mask row (plain: ALLOWED; table complement: NOT-ALLOWED = -1)
+    if (MODE != MODE_CSRCH) {
+        for (int64_t t = ms + gt; t < me; t += GT) {
+            int32_t j = p.m_idx[t];
+            uint32_t h = fib_hash(j, cap_lg);
+            for (;;) {
+                int32_t old = atomicCAS(&tb.keys[h], EMPTY_KEY, j);
+                if (old == EMPTY_KEY) break;
+                h = (h + 1) & cmask;
+            }
+            if (MODE == MODE_CTAB) tb.cnt[h] = -1;
+        }
+        group_bar(bar_id, GT);
+    }
+
+    // 3. products
+    if (KIND == 2) {
+        // ordered float64: one warp (GW == 1), k ascending, lanes over B_k
+        const double* av_p = (const double*)p.a_val;
+        const double* bv_p = (const double*)p.b_val;
+        double* vals = (double*)tb.val;
+        for (int64_t tb0 = as; tb0 < ae; tb0 += 32) {
+            int64_t t = tb0 + lane;
+            int64_t bs = 0, be = 0;
+            double av = 0.0;
+            if (t < ae) {
+                int32_t k = p.a_idx[t];
+                bs = p.b_ptr[k];
+                be = p.b_ptr[k + 1];
+                av = av_p[t];
+            }
+            int nb = (int)min((int64_t)32, ae - tb0);
+            for (int q = 0; q < nb; q++) {
+                int64_t s0 = shfl64(bs, q), s1 = shfl64(be, q);
+                double a = __shfl_sync(FULL, av, q);
+                for (int64_t s = s0 + lane; s < s1; s += 32) {
+                    int32_t j = p.b_idx[s];
+                    int h;
+                    if (MODE == MODE_PLAIN) {
+                        h = probe_find(tb.keys, j, cap_lg, cmask);
+                        if (h < 0) continue;
+                    } else {
+                        if (MODE == MODE_CSRCH && contains_sorted(p.m_idx + ms, me - ms, j)) continue;
+                        h = probe_insert(tb.keys, j, cap_lg, cmask);
+                        if (tb.cnt[h] < 0) continue;
+                    }
+                    evaluated++;
+                    if (NUMERIC) {
+                        double prod = a * bv_p[s];
+                        if (tb.cnt[h] == 0) { vals[h] = prod; tb.cnt[h] = 1; }
+                        else vals[h] += prod;
+                    } else {
+                        tb.cnt[h] = 1;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // order-free integer accumulation over a flattened (k, s) space
+        for (int64_t tb0 = as + 32 * wg; tb0 < ae; tb0 += 32 * GW) {
+            int64_t t = tb0 + lane;
+            int64_t bs = 0;
+            int len = 0;
+            long long av = 0;
+            if (t < ae) {
+                int32_t k = p.a_idx[t];
+                bs = p.b_ptr[k];
+                len = (int)(p.b_ptr[k + 1] - bs);
+                if (KIND == 1) av = ((const long long*)p.a_val)[t];
+            }
+            int incl = warp_incl_scan(len, lane);
+            int total = __shfl_sync(FULL, incl, 31);
+            int excl = incl - len;
+            constexpr int U = 4;
+            for (int base = 0; base < total; base += 32 * U) {
+                int32_t jj[U];
+                int64_t ss[U];
+                long long aa[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    int q = base + 32 * u + lane;
+                    int qc = q < total ? q : total - 1;
+                    int own = owner_of(incl, qc);
+                    int64_t bso = shfl64(bs, own);
+                    int exo = __shfl_sync(FULL, excl, own);
+                    if (KIND == 1) aa[u] = __shfl_sync(FULL, av, own);
+                    ss[u] = bso + (q - exo);
+                    jj[u] = q < total ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (jj[u] == EMPTY_KEY) continue;
+                    int32_t j = jj[u];
+                    int h;
+                    if (MODE == MODE_PLAIN) {
+                        h = probe_find(tb.keys, j, cap_lg, cmask);
+                        if (h < 0) continue;
+                    } else {
+                        if (MODE == MODE_CSRCH && contains_sorted(p.m_idx + ms, me - ms, j)) continue;
+                        h = probe_insert(tb.keys, j, cap_lg, cmask);
+                        if (tb.cnt[h] < 0) continue;
+                    }
+                    evaluated++;
+                    if (KIND == 0) {
+                        if (NUMERIC) atomicAdd(&tb.cnt[h], 1);
+                        else tb.cnt[h] = 1;
+                    } else {
+                        if (NUMERIC) {
+                            long long prod = aa[u] * ((const long long*)p.b_val)[ss[u]];
+                            atomicAdd(&tb.val[h], (unsigned long long)prod);
+                        }
+                        tb.cnt[h] = 1;
+                    }
+                }
+            }
+        }
+    }
+    group_bar(bar_id, GT);
+
+    // 4. gather
+    const int64_t w = NUMERIC ? o.off[i] : 0;
+    int running = 0;
+    if (MODE == MODE_PLAIN) {
+        // mask order, like the reference's gather (_kernels.py:78-85,208-216)
+        for (int64_t base = ms; base < me; base += GT) {
+            int64_t t = base + gt;
+            bool set = false;
+            int32_t j = 0;
+            int h = 0;
+            if (t < me) {
+                j = p.m_idx[t];
+                h = probe_find(tb.keys, j, cap_lg, cmask);
+                set = tb.cnt[h] > 0;
+            }
+            int tot;
+            int pos = group_prefix<GW>(set, &tot, s_warp, bar_id, gt);
+            if (NUMERIC && set) {
+                int64_t d = w + running + pos;
+                o.idx[d] = j;
+                if (KIND == 0) {
+                    if (o.out_f64) ((double*)o.val)[d] = (double)tb.cnt[h];
+                    else ((long long*)o.val)[d] = tb.cnt[h];
+                } else {
+                    ((unsigned long long*)o.val)[d] = tb.val[h];
+                }
+            }
+            running += tot;
+        }
+    } else {
+        // complement: emit inserted keys in column order (_kernels.py:69,198)
+        // count, then bitonic-sort the table by key with invalid slots last
+        int mine = 0;
+        for (int e = gt; e < cap; e += GT) {
+            bool v = tb.keys[e] != EMPTY_KEY && tb.cnt[e] > 0;
+            mine += v;
+            if (NUMERIC && !v) tb.keys[e] = 0x7fffffff;
+        }
+        int tot;
+        // reuse group_prefix as a reduction: every thread contributes `mine`
+        {
+            int acc = mine;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(FULL, acc, d);
+            if (GW == 1) {
+                tot = acc;
+            } else {
+                if (lane == 0) s_warp[wg] = acc;
+                group_bar(bar_id, GT);
+                tot = 0;
+#pragma unroll
+                for (int q = 0; q < GW; q++) tot += s_warp[q];
+            }
+            group_bar(bar_id, GT);
+        }
+        if (NUMERIC && tot > 0) {
+            for (int kk = 2; kk <= cap; kk <<= 1) {
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                    for (int e = gt; e < cap; e += GT) {
+                        int prt = e ^ jj;
+                        if (prt > e) {
+                            bool up = (e & kk) == 0;
+                            int32_t ke = tb.keys[e], kp = tb.keys[prt];
+                            if ((ke > kp) == up) {
+                                tb.keys[e] = kp;
+                                tb.keys[prt] = ke;
+                                int32_t c = tb.cnt[e];
+                                tb.cnt[e] = tb.cnt[prt];
+                                tb.cnt[prt] = c;
+                                if (KIND != 0) {
+                                    unsigned long long v = tb.val[e];
+                                    tb.val[e] = tb.val[prt];
+                                    tb.val[prt] = v;
+                                }
+                            }
+                        }
+                    }
+                    group_bar(bar_id, GT);
+                }
+            }
+            for (int e = gt; e < tot; e += GT) {
+                int64_t d = w + e;
+                o.idx[d] = tb.keys[e];
+                if (KIND == 0) {
+                    if (o.out_f64) ((double*)o.val)[d] = (double)tb.cnt[e];
+                    else ((long long*)o.val)[d] = tb.cnt[e];
+                } else {
+                    ((unsigned long long*)o.val)[d] = tb.val[e];
+                }
+            }
+        }
+        running = tot;
+    }
+    if (gt == 0) o.row_nnz[i] = running;
+    group_bar(bar_id, GT);
+}
+
+// ---------------------------------------------------------------------------
+// Kernel: groups of GW warps fetch rows of one bin dynamically.
+// SMEM: table in dynamic shared memory (groups_per_block * 2^cap_lg_max entries)
+// otherwise in `gslab` (one slab of 2^cap_lg_max entries per group).
+// ---------------------------------------------------------------------------
+template <int GW, bool SMEM, int KIND, int MODE, bool NUMERIC>
+__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256))
+k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
+            unsigned char* gslab) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_row[16];
+    __shared__ int s_warp[32];
+    constexpr int GT = GW * 32;
+    const int groups = blockDim.x / GT;
+    const int g = threadIdx.x / GT;
+    const int gt = threadIdx.x % GT;
+    const int bar_id = 1 + g;
+    const int cap_max = 1 << cap_lg_max;
+    unsigned char* base = SMEM ? smem + (size_t)g * cap_max * HashEntry<KIND>::bytes
+                               : gslab + ((size_t)blockIdx.x * groups + g) * (size_t)cap_max *
+                                             HashEntry<KIND>::bytes;
+    Table<KIND> tb;
+    tb.bind(base, cap_max);
+    unsigned long long evaluated = 0;
+    for (;;) {
+        if (gt == 0) s_row[g] = atomicAdd(wk.cursor, 1);
+        group_bar(bar_id, GT);
+        int r = s_row[g];
+        group_bar(bar_id, GT);
+        if (r >= wk.count) break;
+        int64_t i = wk.rows[r];
+        hash_row<GW, KIND, MODE, NUMERIC>(p, o, tb, i, row_cap_lg[i], gt, bar_id,
+                                          s_warp + g * GW, evaluated);
+    }
+    if (NUMERIC) {
+        long long e = warp_sum_ll((long long)evaluated);
+        if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);
+    }
+}
+
+}  // namespace mm

@@ -1,0 +1,132 @@
+// Exclusive scan (row-pointer build), 1P compaction and reductions.
+//
+// Reference: np.cumsum into out_ptr (multiply.py:366-367, 380-381, 391-392),
+// compact_rows (_kernels.py:586-594), the one-phase bound assertion
+// (multiply.py:390) and the triangle-count reduction (graphs.py:96).
+#pragma once
+#include "common.cuh"
+
+namespace mm {
+
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+// Block-local inclusive scan of `in` (n items) written to out[0..n);
+// each block's total goes to partials[blockIdx.x].
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile(const int64_t* in, int64_t n,
+                                                            int64_t* out, int64_t* partials) {
+    __shared__ long long s_warp[32];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    long long v[SCAN_ITEMS];
+    long long run = 0;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; q++) {
+        int64_t idx = base + q;
+        run += idx < n ? in[idx] : 0;
+        v[q] = run;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long x = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        long long u = __shfl_up_sync(FULL, x, d);
+        if (lane >= d) x += u;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        long long y = s_warp[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            long long u = __shfl_up_sync(FULL, y, d);
+            if (lane >= d) y += u;
+        }
+        s_warp[lane] = y;
+    }
+    __syncthreads();
+    long long prefix = (x - run) + (warp > 0 ? s_warp[warp - 1] : 0);
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; q++) {
+        int64_t idx = base + q;
+        if (idx < n) out[idx] = v[q] + prefix;
+    }
+    if (threadIdx.x == SCAN_THREADS - 1) partials[blockIdx.x] = s_warp[31];
+}
+
+// out[i] += offsets[block of i] (offsets = exclusive scan of the partials).
+__global__ void k_scan_add(int64_t* out, int64_t n, const int64_t* offsets) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < n) out[idx] += offsets[idx / SCAN_TILE];
+}
+
+__global__ void k_set_zero_i64(int64_t* p) { *p = 0; }
+
+// compact_rows with the bound assertion folded in: a row that overran its
+// slot range raises flag (status MM_ERR_INTERNAL at the ABI).
+template <typename T>
+__global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* bounds_off,
+                                                 const int64_t* row_nnz, const int32_t* tmp_idx,
+                                                 const T* tmp_val, const int64_t* out_ptr,
+                                                 int32_t* out_idx, T* out_val, int* flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // each warp takes 32 consecutive rows; lanes cooperate row by row
+    for (int64_t r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
+        int64_t my = r0 + lane;
+        int64_t cnt = 0, src = 0, dst = 0;
+        if (my < nrows) {
+            cnt = row_nnz[my];
+            src = bounds_off[my];
+            dst = out_ptr[my];
+            if (cnt > bounds_off[my + 1] - src) atomicExch(flag, 1);
+        }
+        unsigned any = __ballot_sync(FULL, cnt > 0);
+        while (any) {
+            int q = __ffs(any) - 1;
+            any &= any - 1;
+            int64_t c = shfl64(cnt, q), s = shfl64(src, q), d = shfl64(dst, q);
+            for (int64_t e = lane; e < c; e += 32) {
+                out_idx[d + e] = tmp_idx[s + e];
+                out_val[d + e] = tmp_val[s + e];
+            }
+        }
+    }
+}
+
+// 2P check: symbolic counts must equal the numeric row sizes (multiply.py:375).
+__global__ void k_check_equal(int64_t n, const int64_t* a, const int64_t* b, int* flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (a[i] != b[i]) atomicExch(flag, 1);
+}
+
+// Deterministic two-pass sum: per-block partials in a fixed grid, then one
+// block folds them in order.
+template <typename T>
+__global__ void __launch_bounds__(256) k_reduce_partial(const T* v, int64_t n, T* partials) {
+    __shared__ T s[256];
+    T acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc += v[i];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int d = 128; d > 0; d >>= 1) {
+        if (threadIdx.x < d) s[threadIdx.x] += s[threadIdx.x + d];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+}
+
+template <typename T>
+__global__ void k_reduce_final(const T* partials, int nparts, T* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        T acc = 0;
+        for (int q = 0; q < nparts; q++) acc += partials[q];
+        *out = acc;
+    }
+}
+
+}  // namespace mm

@@ -1,0 +1,131 @@
+"""Row partitioning of the masked multiply across GPUs (one process per GPU).
+
+Rows of C are independent (the reference computes each output row from A_i,
+M_i and the referenced B rows only: multiply.py:8-11), so the multi-GPU form
+is a row-block partition:
+
+* A and M are cut into contiguous row blocks of balanced masked work
+  (w_i = flops_i + nnz(M_i), prefix-sum cuts — ``balanced_cuts``);
+* B is replicated: rank 0 broadcasts it once over NCCL (NVLink/NVSwitch);
+* each rank multiplies its block with no data-path collective;
+* C row blocks concatenate (``concat_row_blocks`` / ``gather_to_rank0``),
+  and the triangle count is an NCCL all-reduce of the per-rank sums.
+
+The partition logic is pure host/torch code and is exercised on CPU with the
+gloo backend (tests/test_distributed_gloo.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .device import DeviceCsr
+
+
+def balanced_cuts(work: np.ndarray, parts: int) -> np.ndarray:
+    """Row cut points [0, c1, ..., nrows] splitting sum(work) into `parts`
+    contiguous blocks of (nearly) equal weight."""
+    work = np.asarray(work, dtype=np.int64)
+    n = work.shape[0]
+    if parts <= 1 or n == 0:
+        return np.array([0, n], dtype=np.int64)
+    cum = np.concatenate([[0], np.cumsum(work)])
+    total = cum[-1]
+    if total == 0:
+        return np.linspace(0, n, parts + 1).astype(np.int64)
+    targets = total * np.arange(1, parts, dtype=np.float64) / parts
+    inner = np.searchsorted(cum, targets, side="left").astype(np.int64)
+    cuts = np.concatenate([[0], np.clip(inner, 0, n), [n]])
+    return np.maximum.accumulate(cuts)
+
+
+def row_work(a_row_ptr: np.ndarray, a_col_idx: np.ndarray, b_row_ptr: np.ndarray,
+             m_row_ptr: np.ndarray) -> np.ndarray:
+    """w_i = flops_i + nnz(M_i) (host numpy; flops_per_row of multiply.py:103-108)."""
+    blen = np.diff(b_row_ptr)
+    per = blen[a_col_idx[: int(a_row_ptr[-1])]]
+    cs = np.zeros(per.size + 1, dtype=np.int64)
+    np.cumsum(per, out=cs[1:])
+    flops = cs[a_row_ptr[1:]] - cs[a_row_ptr[:-1]]
+    return flops + np.diff(m_row_ptr)
+
+
+def row_block(m: DeviceCsr, lo: int, hi: int) -> DeviceCsr:
+    """Rows [lo, hi) of a device CSR as a standalone CSR (views + rebased ptr)."""
+    p0 = int(m.ptr[lo].item())
+    p1 = int(m.ptr[hi].item())
+    ptr = m.ptr[lo: hi + 1] - p0
+    vals = m.values[p0:p1] if m.values is not None else None
+    return DeviceCsr(hi - lo, m.ncols, ptr.contiguous(), m.idx[p0:p1], vals)
+
+
+def concat_row_blocks(parts: list[DeviceCsr]) -> DeviceCsr:
+    """Stack row blocks (in order) into one CSR."""
+    offs = [0]
+    for p in parts:
+        offs.append(offs[-1] + p.nnz)
+    ptrs = [parts[0].ptr[:1]] + [p.ptr[1:] + off for p, off in zip(parts, offs[:-1])]
+    ptr = torch.cat(ptrs)
+    idx = torch.cat([p.idx for p in parts])
+    vals = None if parts[0].values is None else torch.cat([p.values for p in parts])
+    return DeviceCsr(sum(p.nrows for p in parts), parts[0].ncols, ptr, idx, vals)
+
+
+def broadcast_csr(m: DeviceCsr | None, src: int, device, meta_dtype=None) -> DeviceCsr:
+    """Replicate a CSR from rank `src` to every rank (NCCL broadcast on GPU,
+    gloo on CPU).  Non-source ranks pass m=None."""
+    rank = dist.get_rank()
+    meta = torch.zeros(5, dtype=torch.int64, device=device)
+    if rank == src:
+        meta[0], meta[1], meta[2] = m.nrows, m.ncols, m.nnz
+        meta[3] = 0 if m.values is None else (2 if m.values.dtype == torch.float64 else 1)
+    dist.broadcast(meta, src)
+    nrows, ncols, nnz, vk = (int(x) for x in meta[:4].tolist())
+    if rank == src:
+        ptr, idx, vals = m.ptr, m.idx, m.values
+    else:
+        ptr = torch.empty(nrows + 1, dtype=torch.int64, device=device)
+        idx = torch.empty(nnz, dtype=torch.int32, device=device)
+        vals = (None if vk == 0 else
+                torch.empty(nnz, dtype=torch.float64 if vk == 2 else torch.int64, device=device))
+    dist.broadcast(ptr, src)
+    if nnz:
+        dist.broadcast(idx, src)
+        if vals is not None:
+            dist.broadcast(vals, src)
+    return DeviceCsr(nrows, ncols, ptr, idx, vals)
+
+
+def allreduce_sum_(t: torch.Tensor) -> torch.Tensor:
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t
+
+
+def gather_to_rank0(part: DeviceCsr, device) -> DeviceCsr | None:
+    """Concatenate every rank's C row block on rank 0 (all_gather of sizes,
+    then point-to-point transfers of the blocks)."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    meta = torch.tensor([part.nrows, part.nnz], dtype=torch.int64, device=device)
+    metas = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta)
+    if rank != 0:
+        dist.send(part.ptr, 0)
+        if part.nnz:
+            dist.send(part.idx, 0)
+            dist.send(part.values, 0)
+        return None
+    parts = [part]
+    for r in range(1, world):
+        nr, nz = (int(x) for x in metas[r].tolist())
+        ptr = torch.empty(nr + 1, dtype=torch.int64, device=device)
+        idx = torch.empty(nz, dtype=torch.int32, device=device)
+        vals = torch.empty(nz, dtype=part.values.dtype, device=device)
+        dist.recv(ptr, r)
+        if nz:
+            dist.recv(idx, r)
+            dist.recv(vals, r)
+        parts.append(DeviceCsr(nr, part.ncols, ptr, idx, vals))
+    return concat_row_blocks(parts)

@@ -1,0 +1,309 @@
+"""Masked multiply drivers: C = M (.) (A B), plain or complemented — on a B200.
+
+Drop-in mirror of the reference's operator API (pkg/src/maskmul/multiply.py):
+``MultiplyPlan`` (:46-81), ``MultiplyStats`` (:84-100), ``PlanError`` (:42),
+``masked_multiply_with_stats`` (:349-403), ``masked_multiply`` (:406),
+``symbolic_phase`` (:411), ``one_phase_multiply`` / ``two_phase_multiply``
+(:422-427), ``inner_product_multiply`` (:430), ``flops_of`` (:111).
+Same names, argument meaning and exceptions (PlanError / SparseError /
+AssertionError for the reference's internal assertions).
+
+Every multiply runs on the GPU through the C ABI (include/maskmul_b200.h):
+host matrices are uploaded (input preparation, like the reference's untimed
+_Prepared), the device computes C, and C comes back as a canonical CsrMatrix
+with int64 indices.  ``multiply_device`` is the device-resident entry point
+(inputs and output stay in HBM).  There is no CPU fallback.
+
+Plan extensions: ``algorithm="auto"`` (per-row push/pull cost model).
+``workers`` and ``grain`` are accepted for compatibility and have no effect on
+the GPU (the reference guarantees results independent of them).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceCsr
+from .semiring import Semiring, arithmetic_semiring
+from .sparse import CscMatrix, CsrMatrix, MaskView, SparseError, to_csr
+
+ALGORITHMS = ("msa", "hash", "mca", "heap", "heapdot", "inner")
+EXTRA_ALGORITHMS = ("auto",)
+PHASES = ("1p", "2p")
+_LABELS = {"msa": "MSA", "hash": "Hash", "mca": "MCA", "heap": "Heap",
+           "heapdot": "HeapDot", "inner": "Inner", "auto": "Auto"}
+
+
+class PlanError(ValueError):
+    """The requested plan cannot execute this multiply."""
+
+
+@dataclass(frozen=True)
+class MultiplyPlan:
+    algorithm: str = "msa"
+    phases: str = "1p"
+    complemented: bool = False
+    semiring: Semiring = field(default_factory=arithmetic_semiring)
+    workers: int = 1
+    grain: int = 64
+    n_inspect: float | None = None
+
+    def __post_init__(self):
+        if self.algorithm not in ALGORITHMS + EXTRA_ALGORITHMS:
+            raise PlanError(f"unknown algorithm {self.algorithm!r}")
+        if self.phases not in PHASES:
+            raise PlanError(f"phases must be one of {PHASES}")
+        if self.workers < 1:
+            raise PlanError("workers must be >= 1")
+        if self.grain < 1:
+            raise PlanError("grain must be >= 1")
+        if self.n_inspect not in (None, 0, 1, math.inf):
+            raise PlanError("n_inspect must be 0, 1 or inf")
+        if self.algorithm == "mca" and self.complemented:
+            raise PlanError("the mask-compressed accumulator does not support complemented masks")
+        if self.algorithm == "inner" and self.complemented:
+            raise PlanError("the inner-product algorithm does not support complemented masks")
+
+    @property
+    def effective_n_inspect(self) -> float:
+        if self.n_inspect is not None:
+            return self.n_inspect
+        return math.inf if self.algorithm == "heapdot" else 1
+
+    def label(self) -> str:
+        return f"{_LABELS[self.algorithm]}-{self.phases.upper()}"
+
+
+@dataclass
+class MultiplyStats:
+    generated_flops: int = 0
+    evaluated_multiplies: int = 0
+    symbolic_seconds: float = 0.0
+    numeric_seconds: float = 0.0
+    assemble_seconds: float = 0.0
+    output_nnz: int = 0
+    workers: int = 1
+    rows_push: int = 0
+    rows_pull: int = 0
+    rows_empty: int = 0
+
+    @property
+    def total_seconds(self) -> float:
+        return self.symbolic_seconds + self.numeric_seconds + self.assemble_seconds
+
+
+# ---------------------------------------------------------------------------
+# handles
+# ---------------------------------------------------------------------------
+
+_handles: dict[int, int] = {}
+_lock = threading.Lock()
+
+
+def _handle(device_index: int) -> int:
+    with _lock:
+        h = _handles.get(device_index)
+        if h is None:
+            lib = _lib.load()
+            hp = C.c_void_p()
+            rc = lib.mm_create(device_index, C.byref(hp))
+            if rc:
+                raise RuntimeError(f"mm_create failed: {_lib.last_error()}")
+            h = hp.value
+            _handles[device_index] = h
+        return h
+
+
+def _raise(rc: int):
+    msg = _lib.last_error()
+    if rc == _lib.MM_ERR_PLAN:
+        raise PlanError(msg)
+    if rc == _lib.MM_ERR_INPUT:
+        raise SparseError(msg)
+    if rc == _lib.MM_ERR_INTERNAL:
+        raise AssertionError(msg)
+    raise RuntimeError(f"CUDA error in maskmul: {msg}")
+
+
+def _plan_t(plan: MultiplyPlan, comp: bool) -> _lib.PlanT:
+    ni = plan.effective_n_inspect
+    return _lib.PlanT(_lib.MM_ALGO[plan.algorithm], 2 if plan.phases == "2p" else 1, int(comp),
+                      int(plan.semiring.kernel_id),
+                      _lib.MM_DTYPE_FLOAT64 if np.dtype(plan.semiring.dtype).kind == "f"
+                      else _lib.MM_DTYPE_INT64,
+                      -1 if ni == math.inf else int(ni))
+
+
+# ---------------------------------------------------------------------------
+# device-resident entry point
+# ---------------------------------------------------------------------------
+
+def multiply_device(mask: DeviceCsr, a: DeviceCsr, b: DeviceCsr, plan: MultiplyPlan,
+                    complemented: bool | None = None, b_csc: DeviceCsr | None = None,
+                    stream: torch.cuda.Stream | None = None):
+    """C = M (.) (A B) with every operand and the result in HBM.
+
+    Returns (DeviceCsr C, MultiplyStats).  ``complemented`` defaults to
+    ``plan.complemented``.  ``b_csc`` (B stored column-major) is required by
+    ``algorithm="inner"`` and enables pull rows under ``"auto"``.
+    """
+    comp = bool(plan.complemented if complemented is None else (complemented or plan.complemented))
+    if comp and plan.algorithm in ("mca", "inner"):
+        raise PlanError(f"the {'mask-compressed accumulator' if plan.algorithm == 'mca' else 'inner-product algorithm'}"
+                        " does not support complemented masks")
+    dev = a.idx.device
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    lib = _lib.load()
+    h = _handle(dev.index if dev.index is not None else torch.cuda.current_device())
+    pt = _plan_t(plan, comp)
+    mm_mask, mm_a, mm_b = mask.mm(), a.mm(), b.mm()
+    mm_bt = b_csc.mm() if b_csc is not None else None
+    nnz = C.c_int64(0)
+    dtype = torch.float64 if pt.dtype == _lib.MM_DTYPE_FLOAT64 else torch.int64
+    stats = MultiplyStats()
+    t0 = time.perf_counter()
+    rc = lib.mm_multiply_begin(h, C.byref(pt), C.byref(mm_mask), C.byref(mm_a), C.byref(mm_b),
+                               C.byref(mm_bt) if mm_bt is not None else None,
+                               C.c_void_p(stream.cuda_stream), C.byref(nnz))
+    if rc:
+        _raise(rc)
+    t1 = time.perf_counter()
+    n = int(nnz.value)
+    with torch.cuda.stream(stream):
+        row_ptr = torch.empty(mask.nrows + 1, dtype=torch.int64, device=dev)
+        col_idx = torch.empty(n, dtype=torch.int32, device=dev)
+        values = torch.empty(n, dtype=dtype, device=dev)
+    st = _lib.StatsT()
+    rc = lib.mm_multiply_end(h, row_ptr.data_ptr(), col_idx.data_ptr() if n else None,
+                             values.data_ptr() if n else None, C.byref(st))
+    if rc:
+        _raise(rc)
+    t2 = time.perf_counter()
+    if plan.phases == "2p":
+        stats.symbolic_seconds, stats.numeric_seconds = t1 - t0, t2 - t1
+    else:
+        stats.numeric_seconds, stats.assemble_seconds = t1 - t0, t2 - t1
+    stats.generated_flops = int(st.generated_flops)
+    stats.evaluated_multiplies = int(st.evaluated_multiplies)
+    stats.output_nnz = int(st.output_nnz)
+    stats.rows_push, stats.rows_pull, stats.rows_empty = (int(st.rows_push), int(st.rows_pull),
+                                                         int(st.rows_empty))
+    stats.workers = plan.workers
+    return DeviceCsr(mask.nrows, mask.ncols, row_ptr, col_idx, values), stats
+
+
+# ---------------------------------------------------------------------------
+# host-facing drop-in API
+# ---------------------------------------------------------------------------
+
+def _check_a(a):
+    if not (hasattr(a, "row_ptr") and hasattr(a, "col_idx") and hasattr(a, "values")):
+        raise SparseError("A must be a CsrMatrix")
+
+
+def _prepare(mask, a, b, plan: MultiplyPlan, device=None):
+    """_Prepared (multiply.py:175-233): validation, dtype casts, uploads."""
+    _check_a(a)
+    comp = bool(plan.complemented or getattr(mask, "complemented", False))
+    if plan.algorithm == "mca" and comp:
+        raise PlanError("the mask-compressed accumulator does not support complemented masks")
+    if plan.algorithm == "inner" and comp:
+        raise PlanError("the inner-product algorithm does not support complemented masks")
+    b_nrows, b_ncols = b.shape
+    if mask.nrows != a.nrows or mask.ncols != b_ncols or a.ncols != b_nrows:
+        raise SparseError(f"dimension mismatch: mask {mask.shape}, A {a.shape}, B {b.shape}")
+    dt = np.dtype(plan.semiring.dtype)
+    need_vals = plan.semiring.kernel_id == 0
+    dm = DeviceCsr.from_host(mask, device=device, with_values=False)
+    da = DeviceCsr.from_host(a, dtype=dt, device=device, with_values=need_vals)
+    is_csc = hasattr(b, "col_ptr")
+    b_csr = to_csr(b) if is_csc else b
+    db = DeviceCsr.from_host(b_csr, dtype=dt, device=device, with_values=need_vals)
+    dbt = None
+    if plan.algorithm in ("inner", "auto"):
+        dbt = (DeviceCsr.from_host(b, dtype=dt, device=device, with_values=need_vals)
+               if is_csc else db.transpose_storage())
+    return dm, da, db, dbt, comp
+
+
+def masked_multiply_with_stats(mask, a, b, plan: MultiplyPlan, device=None):
+    dm, da, db, dbt, comp = _prepare(mask, a, b, plan, device)
+    c, stats = multiply_device(dm, da, db, plan, complemented=comp, b_csc=dbt)
+    host = c.to_host()
+    host.values = host.values.astype(np.dtype(plan.semiring.dtype), copy=False)
+    return host, stats
+
+
+def masked_multiply(mask, a, b, plan: MultiplyPlan, device=None) -> CsrMatrix:
+    c, _ = masked_multiply_with_stats(mask, a, b, plan, device)
+    return c
+
+
+def symbolic_phase(mask, a, b, plan: MultiplyPlan, device=None) -> np.ndarray:
+    """Exact per-row output nnz (multiply.py:411-419), computed on the GPU."""
+    dm, da, db, dbt, comp = _prepare(mask, a, b, plan, device)
+    dev = da.idx.device
+    stream = torch.cuda.current_stream(dev)
+    counts = torch.zeros(max(mask.nrows, 1), dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    h = _handle(dev.index)
+    pt = _plan_t(plan, comp)
+    mm_bt = dbt.mm() if dbt is not None else None
+    rc = lib.mm_symbolic(h, C.byref(pt), C.byref(dm.mm()), C.byref(da.mm()), C.byref(db.mm()),
+                         C.byref(mm_bt) if mm_bt is not None else None,
+                         C.c_void_p(stream.cuda_stream), counts.data_ptr())
+    if rc:
+        _raise(rc)
+    return counts[: mask.nrows].cpu().numpy()
+
+
+def one_phase_multiply(mask, a, b, plan: MultiplyPlan) -> CsrMatrix:
+    return masked_multiply(mask, a, b, replace(plan, phases="1p"))
+
+
+def two_phase_multiply(mask, a, b, plan: MultiplyPlan) -> CsrMatrix:
+    return masked_multiply(mask, a, b, replace(plan, phases="2p"))
+
+
+def inner_product_multiply(mask, a, b, semiring: Semiring, workers: int = 1) -> CsrMatrix:
+    return masked_multiply(mask, a, b, MultiplyPlan(algorithm="inner", semiring=semiring,
+                                                    workers=workers))
+
+
+def flops_of(a, b, device=None) -> int:
+    """Classical flops(A B) (multiply.py:111-112), counted on the GPU."""
+    _check_a(a)
+    b_csr = to_csr(b) if hasattr(b, "col_ptr") else b
+    da = DeviceCsr.from_host(a, device=device, with_values=False)
+    db = DeviceCsr.from_host(b_csr, device=device, with_values=False)
+    dev = da.idx.device
+    out = torch.zeros(max(a.nrows, 1), dtype=torch.int64, device=dev)
+    tot = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    rc = _lib.load().mm_row_flops(C.byref(da.mm()), C.byref(db.mm()), out.data_ptr(),
+                                  tot.data_ptr(), C.c_void_p(stream.cuda_stream))
+    if rc:
+        _raise(rc)
+    return int(tot.item())
+
+
+def reduce_sum(values: torch.Tensor) -> torch.Tensor:
+    """Deterministic device sum (the triangle-count reduction, graphs.py:96)."""
+    dev = values.device
+    out = torch.zeros(1, dtype=values.dtype, device=dev)
+    dt = _lib.MM_DTYPE_FLOAT64 if values.dtype == torch.float64 else _lib.MM_DTYPE_INT64
+    rc = _lib.load().mm_reduce_sum(values.data_ptr() if values.numel() else None, values.numel(),
+                                   dt, out.data_ptr(),
+                                   C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    if rc:
+        _raise(rc)
+    return out
