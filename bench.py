@@ -38,8 +38,10 @@ sys.path.insert(0, ROOT)
 METRIC = "masked-SpGEMM useful GFLOP/s & triangles/s; HBM GB/s vs roofline at 1/2/4/8 B200"
 UNIT = "useful GFLOP/s"
 EXPECTED_TRIANGLES = {20: 423909251}
-SUMMARY_BYTES = 184          # sizeof(mm::Summary), read back twice per multiply
+SUMMARY_BYTES = 320          # sizeof(mm::Summary), read back twice per multiply
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
+BIN_NAMES = (["empty"] + [f"{m}_t{t}" for m in ("plain", "ctab", "csrch") for t in range(4)]
+             + ["pull", "msa", "mca", "heap"])
 
 
 def parse():
@@ -301,6 +303,12 @@ def run_ours(args, rank, world, local_rank):
     else:
         ms_max, evaluated, flops, nnz_c = my_ms, evaluated_local, flops_local, nnz_c_local
     per = [p / args.steps for p in phase]
+    nb = 17
+    b_rows = (C.c_int64 * nb)()
+    b_flops = (C.c_int64 * nb)()
+    lib.mm_profile_bins(h, b_rows, b_flops, nb)
+    bins = {BIN_NAMES[b]: {"rows": int(b_rows[b]), "flops": int(b_flops[b])}
+            for b in range(nb) if b_rows[b]}
 
     # ---- e2e through the public API from pinned host buffers ----
     e2e = None
@@ -394,6 +402,7 @@ def run_ours(args, rank, world, local_rank):
                          "step_frac": bytes_alg / (ms_max * 1e-3) / 1e9 / peak},
             "phase_ms": {"analyze": per[0], "scatter": per[1], "numeric": per[2],
                          "scan_readback": per[3], "compact": per[4], "multiply_total": per[5]},
+            "bins": bins,
             "gpu_launches": n_launch_total,
             "clocks": clk,
             "wall_s_timed": t_wall,

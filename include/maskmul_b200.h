@@ -132,6 +132,9 @@ int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void
  * number of kernels the library launched for it. */
 int mm_profile_enable(mm_handle_t* h, int on);
 int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
+/* Rows and generated flops per kernel bin of the last multiply (bin ids in
+ * DESIGN.md §4); returns the number of bins. */
+int mm_profile_bins(mm_handle_t* h, int64_t* rows, int64_t* flops, int n);
 
 /* symbolic_phase (multiply.py:411-419): exact per-row output counts into the
  * device array counts[mask->nrows] (int64).  Synchronous on `stream`. */

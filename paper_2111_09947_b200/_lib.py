@@ -18,7 +18,8 @@ MM_DTYPE_INT64, MM_DTYPE_FLOAT64 = 0, 1
 # every symbol declared in include/maskmul_b200.h
 EXPORTS = ("mm_abi_version", "mm_last_error", "mm_create", "mm_destroy", "mm_multiply_begin",
            "mm_multiply_end", "mm_symbolic", "mm_row_flops", "mm_exclusive_scan",
-           "mm_compact_rows", "mm_reduce_sum", "mm_profile_enable", "mm_profile_read")
+           "mm_compact_rows", "mm_reduce_sum", "mm_profile_enable", "mm_profile_read",
+           "mm_profile_bins")
 
 
 class MatrixT(C.Structure):
@@ -64,6 +65,7 @@ def load(path: str | None = None):
     lib.mm_reduce_sum.argtypes = [P, C.c_int64, C.c_int, P, P]
     lib.mm_profile_enable.argtypes = [P, C.c_int]
     lib.mm_profile_read.argtypes = [P, P, C.c_int, C.POINTER(C.c_int64)]
+    lib.mm_profile_bins.argtypes = [P, P, P, C.c_int]
     for name in EXPORTS:
         getattr(lib, name)
         if name not in ("mm_last_error",):

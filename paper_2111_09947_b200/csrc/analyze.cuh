@@ -43,6 +43,7 @@ struct Summary {
     unsigned long long bound_total;
     unsigned long long evaluated;
     long long total_nnz;
+    unsigned long long bin_flops[NBINS];
     int bin_count[NBINS];
     int bin_cap_lg[NBINS];
     int max_na;
@@ -128,9 +129,10 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
                                                  Summary* s) {
     __shared__ int s_count[NBINS];
     __shared__ int s_cap[NBINS];
+    __shared__ unsigned long long s_bflops[NBINS];
     __shared__ unsigned long long s_flops, s_bound;
     __shared__ int s_na, s_nm;
-    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) { s_count[b] = 0; s_cap[b] = 0; }
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) { s_count[b] = 0; s_cap[b] = 0; s_bflops[b] = 0; }
     if (threadIdx.x == 0) { s_flops = 0; s_bound = 0; s_na = 0; s_nm = 0; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
             row_bin[i] = (uint8_t)b;
             row_cap_lg[i] = (int8_t)cap_lg;
             atomicAdd(&s_count[b], 1);
+            atomicAdd(&s_bflops[b], (unsigned long long)f);
             atomicMax(&s_cap[b], cap_lg);
             atomicMax(&s_na, (int)(na < 0x7fffffff ? na : 0x7fffffff));
             atomicMax(&s_nm, (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
@@ -182,6 +185,7 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
     for (int b = threadIdx.x; b < NBINS; b += blockDim.x) {
         if (s_count[b]) {
             atomicAdd(&s->bin_count[b], s_count[b]);
+            atomicAdd(&s->bin_flops[b], s_bflops[b]);
             atomicMax(&s->bin_cap_lg[b], s_cap[b]);
         }
     }

@@ -557,6 +557,15 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches) {
     return MM_OK;
 }
 
+int mm_profile_bins(mm_handle_t* h, int64_t* rows, int64_t* flops, int n) {
+    if (!h) return fail(MM_ERR_INPUT, "null handle");
+    for (int b = 0; b < n && b < NBINS; b++) {
+        if (rows) rows[b] = h->sum.bin_count[b];
+        if (flops) flops[b] = (int64_t)h->sum.bin_flops[b];
+    }
+    return NBINS;
+}
+
 int mm_symbolic(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
                 const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* counts) {
     if (!h || !counts) return fail(MM_ERR_INPUT, "null argument");
@@ -646,12 +655,12 @@ int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* str
         ++g_launches;
         k_reduce_partial<double><<<nparts, 256, 0, st>>>((const double*)values, n, (double*)partials);
         ++g_launches;
-        k_reduce_final<double><<<1, 32, 0, st>>>((const double*)partials, nparts, (double*)out);
+        k_reduce_final<double><<<1, 256, 0, st>>>((const double*)partials, nparts, (double*)out);
     } else {
         ++g_launches;
         k_reduce_partial<long long><<<nparts, 256, 0, st>>>((const long long*)values, n, (long long*)partials);
         ++g_launches;
-        k_reduce_final<long long><<<1, 32, 0, st>>>((const long long*)partials, nparts, (long long*)out);
+        k_reduce_final<long long><<<1, 256, 0, st>>>((const long long*)partials, nparts, (long long*)out);
     }
     cudaFreeAsync(partials, st);
     CU(cudaGetLastError());

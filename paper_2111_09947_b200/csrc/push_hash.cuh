@@ -108,6 +108,36 @@ __device__ __forceinline__ T load_val(const void* p, int64_t i) {
     return ((const T*)p)[i];
 }
 
+// Locate the slot a product with column j accumulates into, or -1 if the
+// mask discards it (plain: j absent; complement: j in the mask).
+template <int MODE, int KIND>
+__device__ __forceinline__ int hash_locate_t(Table<KIND>& tb, int32_t j, int lg, uint32_t cmask,
+                                             const int32_t* mrow, int64_t nm) {
+    if (MODE == MODE_PLAIN) {
+        const int h = probe_find(tb.keys, j, lg, cmask);
+        return h < 0 ? -1 : h;
+    }
+    if (MODE == MODE_CSRCH && contains_sorted(mrow, nm, j)) return -1;
+    const int h = probe_insert(tb.keys, j, lg, cmask);
+    return tb.cnt[h] < 0 ? -1 : h;
+}
+
+// Order-free accumulation of one surviving product into slot h.
+template <int KIND, bool NUMERIC>
+__device__ __forceinline__ void hash_accumulate(Table<KIND>& tb, int h, long long a,
+                                                const void* b_val, int64_t s) {
+    if (KIND == 0) {
+        if (NUMERIC) atomicAdd(&tb.cnt[h], 1);
+        else tb.cnt[h] = 1;
+    } else {
+        if (NUMERIC) {
+            const long long prod = a * ((const long long*)b_val)[s];
+            atomicAdd(&tb.val[h], (unsigned long long)prod);
+        }
+        tb.cnt[h] = 1;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // The row processor.
 // ---------------------------------------------------------------------------
@@ -189,62 +219,79 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             }
         }
     } else {
-        // order-free integer accumulation over a flattened (k, s) space
-        for (int64_t tb0 = as + 32 * wg; tb0 < ae; tb0 += 32 * GW) {
-            int64_t t = tb0 + lane;
+        // Order-free integer accumulation.  Every warp of the group walks the
+        // same batches of 32 A entries; the batch's products are cut into
+        // chunks dealt round-robin to the group's warps (chunk_ctr is
+        // identical in every warp), so a row is balanced across the group no
+        // matter how few A entries it has.
+        //   long B rows (>= 32 entries): warp-wide chunks of 32*U products,
+        //     U independent 4-byte loads in flight per lane;
+        //   short B rows: flattened into 32-wide windows, the owning A entry of
+        //     each lane found by a shuffle binary search over the lengths.
+        constexpr int U = 4;
+        constexpr int CH = 32 * U;
+        int chunk_ctr = 0;
+        for (int64_t tb0 = as; tb0 < ae; tb0 += 32) {
+            const int64_t t = tb0 + lane;
             int64_t bs = 0;
             int len = 0;
             long long av = 0;
             if (t < ae) {
-                int32_t k = p.a_idx[t];
+                const int32_t k = p.a_idx[t];
                 bs = p.b_ptr[k];
                 len = (int)(p.b_ptr[k + 1] - bs);
                 if (KIND == 1) av = ((const long long*)p.a_val)[t];
             }
-            int incl = warp_incl_scan(len, lane);
-            int total = __shfl_sync(FULL, incl, 31);
-            int excl = incl - len;
-            constexpr int U = 4;
-            for (int base = 0; base < total; base += 32 * U) {
-                int32_t jj[U];
-                int64_t ss[U];
-                long long aa[U];
+            unsigned longm = __ballot_sync(FULL, len >= 32);
+            while (longm) {
+                const int l = __ffs(longm) - 1;
+                longm &= longm - 1;
+                const int64_t sb = shfl64(bs, l);
+                const int sl = __shfl_sync(FULL, len, l);
+                const long long sa = KIND == 1 ? __shfl_sync(FULL, av, l) : 0;
+                const int nch = (sl + CH - 1) / CH;
+                const int c0 = (wg - chunk_ctr % GW + GW) % GW;
+                for (int c = c0; c < nch; c += GW) {
+                    const int off = c * CH + lane;
+                    int32_t jj[U];
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    int q = base + 32 * u + lane;
-                    int qc = q < total ? q : total - 1;
-                    int own = owner_of(incl, qc);
-                    int64_t bso = shfl64(bs, own);
-                    int exo = __shfl_sync(FULL, excl, own);
-                    if (KIND == 1) aa[u] = __shfl_sync(FULL, av, own);
-                    ss[u] = bso + (q - exo);
-                    jj[u] = q < total ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
-                }
+                    for (int u = 0; u < U; u++) {
+                        const int o = off + 32 * u;
+                        jj[u] = o < sl ? __ldg(p.b_idx + sb + o) : EMPTY_KEY;
+                    }
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    if (jj[u] == EMPTY_KEY) continue;
-                    int32_t j = jj[u];
-                    int h;
-                    if (MODE == MODE_PLAIN) {
-                        h = probe_find(tb.keys, j, cap_lg, cmask);
+                    for (int u = 0; u < U; u++) {
+                        if (jj[u] == EMPTY_KEY) continue;
+                        const int h = hash_locate_t<MODE, KIND>(tb, jj[u], cap_lg, cmask, p.m_idx + ms, me - ms);
                         if (h < 0) continue;
-                    } else {
-                        if (MODE == MODE_CSRCH && contains_sorted(p.m_idx + ms, me - ms, j)) continue;
-                        h = probe_insert(tb.keys, j, cap_lg, cmask);
-                        if (tb.cnt[h] < 0) continue;
-                    }
-                    evaluated++;
-                    if (KIND == 0) {
-                        if (NUMERIC) atomicAdd(&tb.cnt[h], 1);
-                        else tb.cnt[h] = 1;
-                    } else {
-                        if (NUMERIC) {
-                            long long prod = aa[u] * ((const long long*)p.b_val)[ss[u]];
-                            atomicAdd(&tb.val[h], (unsigned long long)prod);
-                        }
-                        tb.cnt[h] = 1;
+                        evaluated++;
+                        hash_accumulate<KIND, NUMERIC>(tb, h, sa, p.b_val, sb + off + 32 * u);
                     }
                 }
+                chunk_ctr += nch;
+            }
+            const int slen = len < 32 ? len : 0;
+            const int incl = warp_incl_scan(slen, lane);
+            const int total = __shfl_sync(FULL, incl, 31);
+            if (total) {
+                const int excl = incl - slen;
+                const int nwin = (total + 31) >> 5;
+                const int w0 = (wg - chunk_ctr % GW + GW) % GW;
+                for (int wi = w0; wi < nwin; wi += GW) {
+                    const int q = (wi << 5) + lane;
+                    const int own = owner_of(incl, q < total ? q : total - 1);
+                    const int64_t so = shfl64(bs, own) + (q - __shfl_sync(FULL, excl, own));
+                    const long long ao = KIND == 1 ? __shfl_sync(FULL, av, own) : 0;
+                    if (q < total) {
+                        const int h = hash_locate_t<MODE, KIND>(tb, __ldg(p.b_idx + so), cap_lg, cmask,
+                                                        p.m_idx + ms, me - ms);
+                        if (h >= 0) {
+                            evaluated++;
+                            hash_accumulate<KIND, NUMERIC>(tb, h, ao, p.b_val, so);
+                        }
+                    }
+                }
+                chunk_ctr += nwin;
             }
         }
     }

@@ -63,7 +63,9 @@ __global__ void k_scan_add(int64_t* out, int64_t n, const int64_t* offsets) {
 __global__ void k_set_zero_i64(int64_t* p) { *p = 0; }
 
 // compact_rows with the bound assertion folded in: a row that overran its
-// slot range raises flag (status MM_ERR_INTERNAL at the ABI).
+// slot range raises flag (status MM_ERR_INTERNAL at the ABI).  A warp takes
+// 32 consecutive rows; long rows are copied warp-wide, short rows are
+// flattened into 32-wide windows (owner lane found by a shuffle search).
 template <typename T>
 __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* bounds_off,
                                                  const int64_t* row_nnz, const int32_t* tmp_idx,
@@ -72,9 +74,8 @@ __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* b
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // each warp takes 32 consecutive rows; lanes cooperate row by row
     for (int64_t r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
-        int64_t my = r0 + lane;
+        const int64_t my = r0 + lane;
         int64_t cnt = 0, src = 0, dst = 0;
         if (my < nrows) {
             cnt = row_nnz[my];
@@ -82,14 +83,28 @@ __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* b
             dst = out_ptr[my];
             if (cnt > bounds_off[my + 1] - src) atomicExch(flag, 1);
         }
-        unsigned any = __ballot_sync(FULL, cnt > 0);
-        while (any) {
-            int q = __ffs(any) - 1;
-            any &= any - 1;
-            int64_t c = shfl64(cnt, q), s = shfl64(src, q), d = shfl64(dst, q);
+        unsigned longm = __ballot_sync(FULL, cnt >= 32);
+        while (longm) {
+            const int q = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int64_t c = shfl64(cnt, q), s = shfl64(src, q), d = shfl64(dst, q);
             for (int64_t e = lane; e < c; e += 32) {
                 out_idx[d + e] = tmp_idx[s + e];
                 out_val[d + e] = tmp_val[s + e];
+            }
+        }
+        const int sc = cnt < 32 ? (int)cnt : 0;
+        const int incl = warp_incl_scan(sc, lane);
+        const int total = __shfl_sync(FULL, incl, 31);
+        const int excl = incl - sc;
+        for (int base = 0; base < total; base += 32) {
+            const int qi = base + lane;
+            const int own = owner_of(incl, qi < total ? qi : total - 1);
+            const int off = qi - __shfl_sync(FULL, excl, own);
+            const int64_t s = shfl64(src, own) + off, d = shfl64(dst, own) + off;
+            if (qi < total) {
+                out_idx[d] = tmp_idx[s];
+                out_val[d] = tmp_val[s];
             }
         }
     }
@@ -121,12 +136,16 @@ __global__ void __launch_bounds__(256) k_reduce_partial(const T* v, int64_t n, T
 }
 
 template <typename T>
-__global__ void k_reduce_final(const T* partials, int nparts, T* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        T acc = 0;
-        for (int q = 0; q < nparts; q++) acc += partials[q];
-        *out = acc;
+__global__ void __launch_bounds__(256) k_reduce_final(const T* partials, int nparts, T* out) {
+    __shared__ T s[256];
+    T acc = 0;
+    for (int q = threadIdx.x; q < nparts; q += blockDim.x) acc += partials[q];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int d = 128; d > 0; d >>= 1) {
+        if (threadIdx.x < d) s[threadIdx.x] += s[threadIdx.x + d];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *out = s[0];
 }
-
 }  // namespace mm

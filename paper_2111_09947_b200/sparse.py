@@ -187,6 +187,18 @@ def _row_ptr_from_rows(nrows: int, rows: np.ndarray) -> np.ndarray:
     return row_ptr
 
 
+def sorted_unique(keys: np.ndarray) -> np.ndarray:
+    """np.unique for int64 keys via sort + adjacent-difference (np.unique's
+    hash path is orders of magnitude slower on large int64 inputs here)."""
+    k = np.sort(np.asarray(keys, dtype=np.int64))
+    if k.size == 0:
+        return k
+    keep = np.empty(k.size, dtype=bool)
+    keep[0] = True
+    np.not_equal(k[1:], k[:-1], out=keep[1:])
+    return k[keep]
+
+
 def from_arrays(nrows: int, ncols: int, rows, cols, vals, dedup=np.add) -> CsrMatrix:
     """Canonical CSR from coordinate arrays; duplicates combined with ``dedup``.
 
@@ -319,5 +331,5 @@ def simple_undirected_graph(a: CsrMatrix) -> CsrMatrix:
     rows, cols = rows[keep], cols[keep]
     n = np.int64(max(a.ncols, 1))
     key = np.concatenate([rows * n + cols, cols * n + rows])
-    key = np.unique(key)
+    key = sorted_unique(key)
     return _pattern_from_sorted_unique_keys(a.nrows, a.ncols, key)

@@ -20,8 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .semiring import arithmetic_semiring, plus_pair_semiring
-from .sparse import (CsrMatrix, degree_sort_relabel, from_arrays,
-                     simple_undirected_graph, tril_strict)
+from .sparse import CsrMatrix, from_arrays, sorted_unique
 
 GRAPH500_PARAMS = (0.57, 0.19, 0.19, 0.05)
 
@@ -58,13 +57,18 @@ def rmat_edges(spec: GeneratorSpec):
     cuts = np.array([a, a + b, a + b + c])
     rng = np.random.default_rng(spec.seed)
     m = spec.nedges
-    src = np.zeros(m, dtype=np.int64)
-    dst = np.zeros(m, dtype=np.int64)
+    wide = spec.scale > 31
+    src = np.zeros(m, dtype=np.int64 if wide else np.uint32)
+    dst = np.zeros(m, dtype=np.int64 if wide else np.uint32)
     for bit in range(spec.scale):
-        quad = np.searchsorted(cuts, rng.random(m), side="right")
-        src |= (quad >> 1).astype(np.int64) << bit
-        dst |= (quad & 1).astype(np.int64) << bit
-    return src, dst
+        r = rng.random(m)
+        # == np.searchsorted(cuts, r, side="right") (generate.py:62): the
+        # number of cut points <= r, computed branch-free in uint8
+        quad = ((r >= cuts[0]).view(np.uint8) + (r >= cuts[1]).view(np.uint8)
+                + (r >= cuts[2]).view(np.uint8))
+        src |= (quad >> 1).astype(src.dtype) << src.dtype.type(bit)
+        dst |= (quad & 1).astype(dst.dtype) << dst.dtype.type(bit)
+    return src.astype(np.int64), dst.astype(np.int64)
 
 
 def erdos_renyi_edges(spec: GeneratorSpec):
@@ -75,15 +79,43 @@ def erdos_renyi_edges(spec: GeneratorSpec):
     return src, dst
 
 
+def _unique_keys(keys: np.ndarray) -> np.ndarray:
+    """Sorted unique int64 keys.  Input preparation only: on a GPU box the
+    sort runs on the device through torch (same set, same order)."""
+    try:
+        import torch
+        if torch.cuda.is_available() and keys.size > (1 << 20):
+            t = torch.from_numpy(np.ascontiguousarray(keys)).cuda()
+            return torch.unique(t, sorted=True).cpu().numpy()
+    except Exception:
+        pass
+    return sorted_unique(keys)
+
+
+def _csr_from_keys(n_rows: int, n_cols: int, key: np.ndarray) -> CsrMatrix:
+    rows = key // n_cols
+    cols = key - rows * n_cols
+    row_ptr = np.zeros(n_rows + 1, dtype=np.int64)
+    row_ptr[1:] = np.cumsum(np.bincount(rows, minlength=n_rows))
+    return CsrMatrix(n_rows, n_cols, row_ptr, cols, np.ones(key.size, dtype=np.int64))
+
+
 def generate(spec: GeneratorSpec) -> CsrMatrix:
     src, dst = rmat_edges(spec) if spec.kind == "rmat" else erdos_renyi_edges(spec)
     n = spec.nrows
-    key = np.unique(src * np.int64(n) + dst)
-    rows = key // n
-    cols = key - rows * n
-    row_ptr = np.zeros(n + 1, dtype=np.int64)
-    row_ptr[1:] = np.cumsum(np.bincount(rows, minlength=n))
-    return CsrMatrix(n, n, row_ptr, cols, np.ones(key.size, dtype=np.int64))
+    return _csr_from_keys(n, n, _unique_keys(src * np.int64(n) + dst))
+
+
+def simple_graph_direct(spec: GeneratorSpec) -> CsrMatrix:
+    """simple_undirected_graph(generate(spec)) in one pass: dedup of the raw
+    edges followed by symmetrise + dedup is the dedup of the symmetrised raw
+    edges, so the result is the identical canonical CSR."""
+    src, dst = rmat_edges(spec) if spec.kind == "rmat" else erdos_renyi_edges(spec)
+    n = np.int64(spec.nrows)
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    key = _unique_keys(np.concatenate([src * n + dst, dst * n + src]))
+    return _csr_from_keys(spec.nrows, spec.nrows, key)
 
 
 # ---------------------------------------------------------------------------
@@ -109,8 +141,21 @@ def cfg1() -> Workload:
 
 
 def triangle_lower(scale: int = 20, degree: float = 16, seed: int = 0) -> CsrMatrix:
-    g = simple_undirected_graph(generate(GeneratorSpec("rmat", scale, degree, seed=seed)))
-    return tril_strict(degree_sort_relabel(g)[0])
+    """tril_strict(degree_sort_relabel(simple_undirected_graph(rmat))[0])
+    (graphs.py:91-92) computed on keys: relabel by non-increasing degree
+    (ties by index, sparse.py:340) and keep new_col < new_row."""
+    g = simple_graph_direct(GeneratorSpec("rmat", scale, degree, seed=seed))
+    n = g.nrows
+    deg = np.diff(g.row_ptr)
+    perm = np.lexsort((np.arange(n), -deg)).astype(np.int64)
+    new_label = np.empty(n, dtype=np.int64)
+    new_label[perm] = np.arange(n, dtype=np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
+    nr = new_label[rows]
+    nc = new_label[g.col_idx]
+    keep = nc < nr
+    key = _unique_keys(nr[keep] * np.int64(n) + nc[keep])
+    return _csr_from_keys(n, n, key)
 
 
 def cfg2(scale: int = 20) -> Workload:
@@ -130,7 +175,7 @@ def cfg3(mask_degree: int) -> Workload:
 
 
 def cfg4() -> Workload:
-    g = simple_undirected_graph(generate(GeneratorSpec("rmat", 18, 16, seed=0)))
+    g = simple_graph_direct(GeneratorSpec("rmat", 18, 16, seed=0))
     n = g.nrows
     rng = np.random.default_rng(4)
     src = rng.choice(n, 512, replace=False)
@@ -153,6 +198,6 @@ def cfg4() -> Workload:
 
 
 def cfg5(scale: int = 22) -> Workload:
-    g = simple_undirected_graph(generate(GeneratorSpec("rmat", scale, 16, seed=0)))
+    g = simple_graph_direct(GeneratorSpec("rmat", scale, 16, seed=0))
     return Workload("cfg5", g.pattern(), g, g, plus_pair_semiring(np.int64), False,
                     f"k-truss support R-MAT s{scale} ef16, C=A.(A A) plus-pair")
