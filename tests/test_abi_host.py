@@ -86,8 +86,11 @@ def test_sparse_constructors_canonical():
 def test_generators_match_reference_digests():
     from paper_2111_09947_b200 import workloads
     k = load_json("kats.json")
-    g = workloads.simple_undirected_graph(
+    from paper_2111_09947_b200.sparse import simple_undirected_graph
+    g = simple_undirected_graph(
         workloads.generate(workloads.GeneratorSpec("erdos-renyi", 10, 8, seed=42)))
+    assert digest_mat(workloads.simple_graph_direct(
+        workloads.GeneratorSpec("erdos-renyi", 10, 8, seed=42))) == k["er10_d8_seed42_graph_digest"]
     assert digest_mat(g) == k["er10_d8_seed42_graph_digest"]
     cfg1 = load_json("configs.json")["cfg1"]
     assert digest_mat(workloads.cfg1().a) == cfg1["digest_a"]
