@@ -245,7 +245,8 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             int cap_lg = std::max(h->sum.bin_cap_lg[b], 5);
             size_t ebytes = kind == 0 ? 8 : 16;
             size_t table = ((size_t)1 << cap_lg) * ebytes;
-            size_t smem = smem_table ? groups * table : 0;
+            size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            size_t smem = (smem_table ? groups * table : 0) + groups * batch;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "hash tier table exceeds shared memory");
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
@@ -434,7 +435,8 @@ int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_value
     int* flag = &h->d_summary->flag;
     if (h->plan.phases == 1) {
         if (m > 0) {
-            int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 16);
+            int64_t want = std::max<int64_t>((h->total_nnz + 2047) / 2048, (m + 255) / 256);
+            int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)h->num_sms * 16));
             ++g_launches;
             if (h->out_f64)
                 k_compact<double><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,

@@ -30,6 +30,13 @@ struct HashEntry {
     static constexpr int bytes = KIND == 0 ? 8 : 16;
 };
 
+// Per-group shared-memory staging of one batch of A entries (order-free kinds):
+// base (8 B) [+ a value (8 B)] + inclusive product end (4 B) per thread.
+template <int GW, int KIND>
+__host__ __device__ constexpr size_t batch_bytes() {
+    return KIND == 2 ? 0 : (size_t)GW * 32 * ((KIND == 1 ? 16 : 8) + 4);
+}
+
 // Pointers into one group's table region.
 template <int KIND>
 struct Table {
@@ -103,9 +110,29 @@ __device__ __forceinline__ int group_prefix(bool flag, int* total, int* s_warp, 
     }
 }
 
-template <typename T>
-__device__ __forceinline__ T load_val(const void* p, int64_t i) {
-    return ((const T*)p)[i];
+// Group-wide inclusive scan of an int (one value per thread); *total = sum.
+template <int GW>
+__device__ __forceinline__ int group_incl_scan(int v, int* total, int* s_warp, int bar_id, int gt) {
+    const int lane = gt & 31;
+    int x = warp_incl_scan(v, lane);
+    if (GW == 1) {
+        *total = __shfl_sync(FULL, x, 31);
+        return x;
+    } else {
+        const int w = gt >> 5;
+        if (lane == 31) s_warp[w] = x;
+        group_bar(bar_id, GW * 32);
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < GW; q++) {
+            const int c = s_warp[q];
+            if (q < w) before += c;
+            tot += c;
+        }
+        group_bar(bar_id, GW * 32);
+        *total = tot;
+        return x + before;
+    }
 }
 
 // Locate the slot a product with column j accumulates into, or -1 if the
@@ -144,6 +171,7 @@ __device__ __forceinline__ void hash_accumulate(Table<KIND>& tb, int h, long lon
 template <int GW, int KIND, int MODE, bool NUMERIC>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, int64_t i,
                                          int cap_lg, int gt, int bar_id, int* s_warp,
+                                         int32_t* bs_incl, long long* bs_base, long long* bs_av,
                                          unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
     const int lane = gt & 31;
@@ -219,80 +247,92 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             }
         }
     } else {
-        // Order-free integer accumulation.  Every warp of the group walks the
-        // same batches of 32 A entries; the batch's products are cut into
-        // chunks dealt round-robin to the group's warps (chunk_ctr is
-        // identical in every warp), so a row is balanced across the group no
-        // matter how few A entries it has.
-        //   long B rows (>= 32 entries): warp-wide chunks of 32*U products,
-        //     U independent 4-byte loads in flight per lane;
-        //   short B rows: flattened into 32-wide windows, the owning A entry of
-        //     each lane found by a shuffle binary search over the lengths.
+        // Order-free integer accumulation over the row's flattened product
+        // space, batch by batch (NB = GT entries of A_i per batch):
+        //   1. thread gt loads A entry tb0+gt: base of its B row and length;
+        //      a group-wide scan gives every product q in the batch a B slot
+        //      s = s_base[l] + q for the entry l with s_incl[l-1] <= q < s_incl[l];
+        //   2. warp w takes the contiguous product range [w P/GW, (w+1) P/GW),
+        //      so every warp gets the same amount of work;
+        //   3. windows of 32*U products: when a window lies inside one B row
+        //      (the common case for long rows) lanes address it directly;
+        //      otherwise each lane binary-searches its entry in s_incl.
         constexpr int U = 4;
-        constexpr int CH = 32 * U;
-        int chunk_ctr = 0;
-        for (int64_t tb0 = as; tb0 < ae; tb0 += 32) {
-            const int64_t t = tb0 + lane;
-            int64_t bs = 0;
+        constexpr int NB = GT;
+        int32_t* s_incl = bs_incl;
+        long long* s_base = bs_base;
+        long long* s_av = bs_av;
+        for (int64_t tb0 = as; tb0 < ae; tb0 += NB) {
+            const int64_t t = tb0 + gt;
+            long long base = 0, av = 0;
             int len = 0;
-            long long av = 0;
             if (t < ae) {
                 const int32_t k = p.a_idx[t];
-                bs = p.b_ptr[k];
-                len = (int)(p.b_ptr[k + 1] - bs);
+                base = p.b_ptr[k];
+                len = (int)(p.b_ptr[k + 1] - base);
                 if (KIND == 1) av = ((const long long*)p.a_val)[t];
             }
-            unsigned longm = __ballot_sync(FULL, len >= 32);
-            while (longm) {
-                const int l = __ffs(longm) - 1;
-                longm &= longm - 1;
-                const int64_t sb = shfl64(bs, l);
-                const int sl = __shfl_sync(FULL, len, l);
-                const long long sa = KIND == 1 ? __shfl_sync(FULL, av, l) : 0;
-                const int nch = (sl + CH - 1) / CH;
-                const int c0 = (wg - chunk_ctr % GW + GW) % GW;
-                for (int c = c0; c < nch; c += GW) {
-                    const int off = c * CH + lane;
+            int tot;
+            const int incl = group_incl_scan<GW>(len, &tot, s_warp, bar_id, gt);
+            s_incl[gt] = incl;
+            s_base[gt] = base - (incl - len);
+            if (KIND == 1) s_av[gt] = av;
+            group_bar(bar_id, GT);
+            const int q_lo = (int)(((long long)tot * wg) / GW);
+            const int q_hi = (int)(((long long)tot * (wg + 1)) / GW);
+            if (q_lo < q_hi) {
+                // first entry whose inclusive end exceeds q_lo
+                int cur = 0;
+                {
+                    int lo = 0, hi = NB - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (s_incl[mid] <= q_lo) lo = mid + 1; else hi = mid;
+                    }
+                    cur = lo;
+                }
+                for (int q0 = q_lo; q0 < q_hi; q0 += 32 * U) {
+                    while (s_incl[cur] <= q0) cur++;
+                    const int qend = min(q0 + 32 * U, q_hi) - 1;
                     int32_t jj[U];
+                    long long ss[U];
+                    long long aa[U];
+                    if (qend < s_incl[cur]) {
+                        const long long bse = s_base[cur];
+                        const long long a0 = KIND == 1 ? s_av[cur] : 0;
 #pragma unroll
-                    for (int u = 0; u < U; u++) {
-                        const int o = off + 32 * u;
-                        jj[u] = o < sl ? __ldg(p.b_idx + sb + o) : EMPTY_KEY;
+                        for (int u = 0; u < U; u++) {
+                            const int q = q0 + 32 * u + (gt & 31);
+                            ss[u] = bse + q;
+                            aa[u] = a0;
+                            jj[u] = q <= qend ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; u++) {
+                            const int q = q0 + 32 * u + (gt & 31);
+                            int lo = cur, hi = NB - 1;
+                            while (lo < hi) {
+                                const int mid = (lo + hi) >> 1;
+                                if (s_incl[mid] <= q) lo = mid + 1; else hi = mid;
+                            }
+                            ss[u] = s_base[lo] + q;
+                            aa[u] = KIND == 1 ? s_av[lo] : 0;
+                            jj[u] = q <= qend ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                        }
                     }
 #pragma unroll
                     for (int u = 0; u < U; u++) {
                         if (jj[u] == EMPTY_KEY) continue;
-                        const int h = hash_locate_t<MODE, KIND>(tb, jj[u], cap_lg, cmask, p.m_idx + ms, me - ms);
+                        const int h = hash_locate_t<MODE, KIND>(tb, jj[u], cap_lg, cmask,
+                                                                p.m_idx + ms, me - ms);
                         if (h < 0) continue;
                         evaluated++;
-                        hash_accumulate<KIND, NUMERIC>(tb, h, sa, p.b_val, sb + off + 32 * u);
+                        hash_accumulate<KIND, NUMERIC>(tb, h, aa[u], p.b_val, ss[u]);
                     }
                 }
-                chunk_ctr += nch;
             }
-            const int slen = len < 32 ? len : 0;
-            const int incl = warp_incl_scan(slen, lane);
-            const int total = __shfl_sync(FULL, incl, 31);
-            if (total) {
-                const int excl = incl - slen;
-                const int nwin = (total + 31) >> 5;
-                const int w0 = (wg - chunk_ctr % GW + GW) % GW;
-                for (int wi = w0; wi < nwin; wi += GW) {
-                    const int q = (wi << 5) + lane;
-                    const int own = owner_of(incl, q < total ? q : total - 1);
-                    const int64_t so = shfl64(bs, own) + (q - __shfl_sync(FULL, excl, own));
-                    const long long ao = KIND == 1 ? __shfl_sync(FULL, av, own) : 0;
-                    if (q < total) {
-                        const int h = hash_locate_t<MODE, KIND>(tb, __ldg(p.b_idx + so), cap_lg, cmask,
-                                                        p.m_idx + ms, me - ms);
-                        if (h >= 0) {
-                            evaluated++;
-                            hash_accumulate<KIND, NUMERIC>(tb, h, ao, p.b_val, so);
-                        }
-                    }
-                }
-                chunk_ctr += nwin;
-            }
+            group_bar(bar_id, GT);
         }
     }
     group_bar(bar_id, GT);
@@ -412,9 +452,15 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
     const int gt = threadIdx.x % GT;
     const int bar_id = 1 + g;
     const int cap_max = 1 << cap_lg_max;
+    constexpr size_t BATCH_BYTES = batch_bytes<GW, KIND>();
     unsigned char* base = SMEM ? smem + (size_t)g * cap_max * HashEntry<KIND>::bytes
                                : gslab + ((size_t)blockIdx.x * groups + g) * (size_t)cap_max *
                                              HashEntry<KIND>::bytes;
+    unsigned char* bbase = smem + (SMEM ? (size_t)groups * cap_max * HashEntry<KIND>::bytes : 0) +
+                           (size_t)g * BATCH_BYTES;
+    long long* bs_base = (long long*)bbase;
+    long long* bs_av = bs_base + GT;
+    int32_t* bs_incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
     Table<KIND> tb;
     tb.bind(base, cap_max);
     unsigned long long evaluated = 0;
@@ -426,7 +472,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
         if (r >= wk.count) break;
         int64_t i = wk.rows[r];
         hash_row<GW, KIND, MODE, NUMERIC>(p, o, tb, i, row_cap_lg[i], gt, bar_id,
-                                          s_warp + g * GW, evaluated);
+                                          s_warp + g * GW, bs_incl, bs_base, bs_av, evaluated);
     }
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);

@@ -62,49 +62,53 @@ __global__ void k_scan_add(int64_t* out, int64_t n, const int64_t* offsets) {
 
 __global__ void k_set_zero_i64(int64_t* p) { *p = 0; }
 
-// compact_rows with the bound assertion folded in: a row that overran its
-// slot range raises flag (status MM_ERR_INTERNAL at the ABI).  A warp takes
-// 32 consecutive rows; long rows are copied warp-wide, short rows are
-// flattened into 32-wide windows (owner lane found by a shuffle search).
+// compact_rows (_kernels.py:586-594), element-parallel: a warp owns 256
+// consecutive OUTPUT entries, finds the row of each by a binary search of
+// out_ptr restricted to the warp's row span, and copies from the row's slot
+// range.  Work is proportional to nnz(C) whatever the row-length skew.  The
+// one-phase bound assertion (multiply.py:390) is checked row-parallel: a row
+// that overran its slot range raises flag (MM_ERR_INTERNAL at the ABI).
 template <typename T>
 __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* bounds_off,
                                                  const int64_t* row_nnz, const int32_t* tmp_idx,
                                                  const T* tmp_val, const int64_t* out_ptr,
                                                  int32_t* out_idx, T* out_val, int* flag) {
     const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
-        const int64_t my = r0 + lane;
-        int64_t cnt = 0, src = 0, dst = 0;
-        if (my < nrows) {
-            cnt = row_nnz[my];
-            src = bounds_off[my];
-            dst = out_ptr[my];
-            if (cnt > bounds_off[my + 1] - src) atomicExch(flag, 1);
-        }
-        unsigned longm = __ballot_sync(FULL, cnt >= 32);
-        while (longm) {
-            const int q = __ffs(longm) - 1;
-            longm &= longm - 1;
-            const int64_t c = shfl64(cnt, q), s = shfl64(src, q), d = shfl64(dst, q);
-            for (int64_t e = lane; e < c; e += 32) {
-                out_idx[d + e] = tmp_idx[s + e];
-                out_val[d + e] = tmp_val[s + e];
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = gtid; i < nrows; i += nthreads)
+        if (row_nnz[i] > bounds_off[i + 1] - bounds_off[i]) atomicExch(flag, 1);
+    const int64_t total = out_ptr[nrows];
+    const int64_t warp = gtid >> 5;
+    const int64_t nwarps = nthreads >> 5;
+    constexpr int PER = 256;
+    for (int64_t e0 = warp * PER; e0 < total; e0 += nwarps * PER) {
+        const int64_t e1 = e0 + PER < total ? e0 + PER : total;
+        // row span of [e0, e1): last row r with out_ptr[r] <= e
+        int64_t r_lo = 0, r_hi = 0;
+        if (lane < 2) {
+            const int64_t e = lane == 0 ? e0 : e1 - 1;
+            int64_t lo = 0, hi = nrows;   // search over out_ptr[0..nrows]
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (out_ptr[mid] <= e) lo = mid; else hi = mid - 1;
             }
+            r_lo = lo;
         }
-        const int sc = cnt < 32 ? (int)cnt : 0;
-        const int incl = warp_incl_scan(sc, lane);
-        const int total = __shfl_sync(FULL, incl, 31);
-        const int excl = incl - sc;
-        for (int base = 0; base < total; base += 32) {
-            const int qi = base + lane;
-            const int own = owner_of(incl, qi < total ? qi : total - 1);
-            const int off = qi - __shfl_sync(FULL, excl, own);
-            const int64_t s = shfl64(src, own) + off, d = shfl64(dst, own) + off;
-            if (qi < total) {
-                out_idx[d] = tmp_idx[s];
-                out_val[d] = tmp_val[s];
+        r_hi = shfl64(r_lo, 1);
+        r_lo = shfl64(r_lo, 0);
+#pragma unroll 4
+        for (int u = 0; u < PER / 32; u++) {
+            const int64_t e = e0 + u * 32 + lane;
+            if (e < e1) {
+                int64_t lo = r_lo, hi = r_hi;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) >> 1;
+                    if (__ldg(out_ptr + mid) <= e) lo = mid; else hi = mid - 1;
+                }
+                const int64_t src = bounds_off[lo] + (e - out_ptr[lo]);
+                out_idx[e] = tmp_idx[src];
+                out_val[e] = tmp_val[src];
             }
         }
     }
