@@ -249,19 +249,20 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     } else {
         // Order-free integer accumulation over the row's flattened product
         // space, batch by batch (NB = GT entries of A_i per batch):
-        //   1. thread gt loads A entry tb0+gt: base of its B row and length;
-        //      a group-wide scan gives every product q in the batch a B slot
-        //      s = s_base[l] + q for the entry l with s_incl[l-1] <= q < s_incl[l];
-        //   2. warp w takes the contiguous product range [w P/GW, (w+1) P/GW),
-        //      so every warp gets the same amount of work;
-        //   3. windows of 32*U products: when a window lies inside one B row
-        //      (the common case for long rows) lanes address it directly;
-        //      otherwise each lane binary-searches its entry in s_incl.
+        //   1. thread gt loads A entry tb0+gt (base of its B row, length); a
+        //      group-wide scan assigns every product q of the batch the B slot
+        //      s_base[l] + q of the entry l with s_incl[l-1] <= q < s_incl[l];
+        //   2. warp w owns the contiguous product range [w P/GW, (w+1) P/GW)
+        //      (equal work per warp) and walks the entries overlapping it,
+        //      32 at a time, one per lane:
+        //        portions >= 32 products: warp-wide chunks of 32*U loads
+        //        (U independent loads in flight per lane), no search;
+        //        shorter portions: flattened into 32-wide windows, the owning
+        //        lane found by a shuffle binary search.
         constexpr int U = 4;
+        constexpr int CH = 32 * U;
         constexpr int NB = GT;
-        int32_t* s_incl = bs_incl;
-        long long* s_base = bs_base;
-        long long* s_av = bs_av;
+        const int lane32 = gt & 31;
         for (int64_t tb0 = as; tb0 < ae; tb0 += NB) {
             const int64_t t = tb0 + gt;
             long long base = 0, av = 0;
@@ -274,55 +275,90 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             }
             int tot;
             const int incl = group_incl_scan<GW>(len, &tot, s_warp, bar_id, gt);
-            s_incl[gt] = incl;
-            s_base[gt] = base - (incl - len);
-            if (KIND == 1) s_av[gt] = av;
-            group_bar(bar_id, GT);
-            const int q_lo = (int)(((long long)tot * wg) / GW);
-            const int q_hi = (int)(((long long)tot * (wg + 1)) / GW);
-            if (q_lo < q_hi) {
-                // first entry whose inclusive end exceeds q_lo
-                int cur = 0;
-                {
-                    int lo = 0, hi = NB - 1;
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (s_incl[mid] <= q_lo) lo = mid + 1; else hi = mid;
-                    }
-                    cur = lo;
+            int q_lo = 0, q_hi = tot;
+            int l_lo = 0, l_end = NB;
+            if (GW > 1) {
+                bs_incl[gt] = incl;
+                bs_base[gt] = base - (incl - len);
+                if (KIND == 1) bs_av[gt] = av;
+                group_bar(bar_id, GT);
+                q_lo = (int)(((long long)tot * wg) / GW);
+                q_hi = (int)(((long long)tot * (wg + 1)) / GW);
+                // entries overlapping [q_lo, q_hi): first with incl > q_lo ...
+                int lo = 0, hi = NB - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (bs_incl[mid] <= q_lo) lo = mid + 1; else hi = mid;
                 }
-                for (int q0 = q_lo; q0 < q_hi; q0 += 32 * U) {
-                    while (s_incl[cur] <= q0) cur++;
-                    const int qend = min(q0 + 32 * U, q_hi) - 1;
-                    int32_t jj[U];
-                    long long ss[U];
-                    long long aa[U];
-                    if (qend < s_incl[cur]) {
-                        const long long bse = s_base[cur];
-                        const long long a0 = KIND == 1 ? s_av[cur] : 0;
+                l_lo = lo;
+                // ... through the first with incl >= q_hi
+                hi = NB - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (bs_incl[mid] < q_hi) lo = mid + 1; else hi = mid;
+                }
+                l_end = lo + 1;
+            }
+            for (int l0 = l_lo; l0 < l_end && q_lo < q_hi; l0 += 32) {
+                // this lane's entry and its portion inside [q_lo, q_hi)
+                const int l = l0 + lane32;
+                long long sb = 0, sa = 0;
+                int plen = 0;
+                if (GW == 1) {
+                    sb = base;
+                    plen = len;
+                    sa = av;
+                } else if (l < l_end) {
+                    const int e_in = bs_incl[l];
+                    const int e_ex = l > 0 ? bs_incl[l - 1] : 0;
+                    const int a0 = e_ex > q_lo ? e_ex : q_lo;
+                    const int a1 = e_in < q_hi ? e_in : q_hi;
+                    plen = a1 > a0 ? a1 - a0 : 0;
+                    sb = bs_base[l] + a0;
+                    if (KIND == 1) sa = bs_av[l];
+                }
+                unsigned longm = __ballot_sync(FULL, plen >= 32);
+                while (longm) {
+                    const int src = __ffs(longm) - 1;
+                    longm &= longm - 1;
+                    const long long b0 = shfl64(sb, src);
+                    const int n0 = __shfl_sync(FULL, plen, src);
+                    const long long a0 = KIND == 1 ? __shfl_sync(FULL, sa, src) : 0;
+                    for (int c = 0; c < n0; c += CH) {
+                        int32_t jj[U];
 #pragma unroll
                         for (int u = 0; u < U; u++) {
-                            const int q = q0 + 32 * u + (gt & 31);
-                            ss[u] = bse + q;
-                            aa[u] = a0;
-                            jj[u] = q <= qend ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                            const int o = c + 32 * u + lane32;
+                            jj[u] = o < n0 ? __ldg(p.b_idx + b0 + o) : EMPTY_KEY;
                         }
-                    } else {
 #pragma unroll
                         for (int u = 0; u < U; u++) {
-                            const int q = q0 + 32 * u + (gt & 31);
-                            int lo = cur, hi = NB - 1;
-                            while (lo < hi) {
-                                const int mid = (lo + hi) >> 1;
-                                if (s_incl[mid] <= q) lo = mid + 1; else hi = mid;
-                            }
-                            ss[u] = s_base[lo] + q;
-                            aa[u] = KIND == 1 ? s_av[lo] : 0;
-                            jj[u] = q <= qend ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                            if (jj[u] == EMPTY_KEY) continue;
+                            const int h = hash_locate_t<MODE, KIND>(tb, jj[u], cap_lg, cmask,
+                                                                    p.m_idx + ms, me - ms);
+                            if (h < 0) continue;
+                            evaluated++;
+                            hash_accumulate<KIND, NUMERIC>(tb, h, a0, p.b_val, b0 + c + 32 * u + lane32);
                         }
                     }
+                }
+                const int slen = plen < 32 ? plen : 0;
+                const int sincl = warp_incl_scan(slen, lane32);
+                const int stot = __shfl_sync(FULL, sincl, 31);
+                const int sexcl = sincl - slen;
+                for (int w0 = 0; w0 < stot; w0 += 64) {
+                    int32_t jj[2];
+                    long long ss[2], aa[2];
 #pragma unroll
-                    for (int u = 0; u < U; u++) {
+                    for (int u = 0; u < 2; u++) {
+                        const int q = w0 + 32 * u + lane32;
+                        const int own = owner_of(sincl, q < stot ? q : stot - 1);
+                        ss[u] = shfl64(sb, own) + (q - __shfl_sync(FULL, sexcl, own));
+                        aa[u] = KIND == 1 ? __shfl_sync(FULL, sa, own) : 0;
+                        jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
                         if (jj[u] == EMPTY_KEY) continue;
                         const int h = hash_locate_t<MODE, KIND>(tb, jj[u], cap_lg, cmask,
                                                                 p.m_idx + ms, me - ms);
@@ -331,8 +367,9 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
                         hash_accumulate<KIND, NUMERIC>(tb, h, aa[u], p.b_val, ss[u]);
                     }
                 }
+                if (GW == 1) break;
             }
-            group_bar(bar_id, GT);
+            if (GW > 1) group_bar(bar_id, GT);
         }
     }
     group_bar(bar_id, GT);
