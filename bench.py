@@ -38,9 +38,10 @@ sys.path.insert(0, ROOT)
 METRIC = "masked-SpGEMM useful GFLOP/s & triangles/s; HBM GB/s vs roofline at 1/2/4/8 B200"
 UNIT = "useful GFLOP/s"
 EXPECTED_TRIANGLES = {20: 423909251}
-SUMMARY_BYTES = 320          # sizeof(mm::Summary), read back twice per multiply
+SUMMARY_BYTES = 464          # sizeof(mm::Summary), read back twice per multiply
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
-BIN_NAMES = (["empty"] + [f"{m}_t{t}" for m in ("plain", "ctab", "csrch") for t in range(4)]
+BIN_NAMES = (["empty"] + [f"{m}_t{t}{c}" for m in ("plain", "ctab", "csrch")
+                          for t, c in ((0, "s"), (0, "l"), (1, "s"), (1, "l"), (2, "s"), (2, "l"), (3, "g"))]
              + ["pull", "msa", "mca", "heap"])
 
 
@@ -303,7 +304,7 @@ def run_ours(args, rank, world, local_rank):
     else:
         ms_max, evaluated, flops, nnz_c = my_ms, evaluated_local, flops_local, nnz_c_local
     per = [p / args.steps for p in phase]
-    nb = 17
+    nb = len(BIN_NAMES)
     b_rows = (C.c_int64 * nb)()
     b_flops = (C.c_int64 * nb)()
     lib.mm_profile_bins(h, b_rows, b_flops, nb)

@@ -17,18 +17,29 @@ enum Family : int { FAM_HASH = 0, FAM_MSA = 1, FAM_MCA = 2, FAM_HEAP = 3, FAM_PU
 // Hash-family modes.
 enum Mode : int { MODE_PLAIN = 0, MODE_CTAB = 1, MODE_CSRCH = 2 };
 
-// Bins.  0 = nothing to compute (row_nnz = 0).
+// Bins.  0 = nothing to compute (row_nnz = 0).  Hash bins: 7 per mode =
+// tiers 0..2 x {small table (<= 2^CAPC_LG slots), large table} + the
+// global-memory tier 3; the table class keeps the shared-memory footprint of
+// a launch (and so its occupancy) sized for the rows it actually holds.
+constexpr int CAPC_LG = 9;
 enum Bin : int {
     BIN_EMPTY = 0,
-    BIN_HASH0 = 1,    // + mode*4 + tier   (tiers 0..3)
-    BIN_PULL = 13,
-    BIN_MSA = 14,
-    BIN_MCA = 15,
-    BIN_HEAP = 16,
-    NBINS = 17
+    BIN_HASH0 = 1,    // + mode*7 + (tier < 3 ? tier*2 + class : 6)
+    BIN_PULL = 22,
+    BIN_MSA = 23,
+    BIN_MCA = 24,
+    BIN_HEAP = 25,
+    NBINS = 26
 };
 
-__host__ __device__ constexpr int hash_bin(int mode, int tier) { return BIN_HASH0 + mode * 4 + tier; }
+__host__ __device__ constexpr int hash_bin(int mode, int tier, int cls) {
+    return BIN_HASH0 + mode * 7 + (tier < 3 ? tier * 2 + cls : 6);
+}
+__host__ __device__ constexpr bool is_hash_bin(int b) { return b >= BIN_HASH0 && b < BIN_HASH0 + 21; }
+__host__ __device__ constexpr int hash_bin_mode(int b) { return (b - BIN_HASH0) / 7; }
+__host__ __device__ constexpr int hash_bin_tier(int b) {
+    return ((b - BIN_HASH0) % 7) == 6 ? 3 : ((b - BIN_HASH0) % 7) / 2;
+}
 
 // Hash tiers: group width (warps) and the largest table (log2 entries) each
 // tier keeps in shared memory.  Tier 3 keeps its table in global memory.
@@ -119,8 +130,9 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         tier = tc > tf ? tc : tf;
     }
     int lim = tier_cap_lg(ap.pair, tier);
-    *cap_lg_out = want < lim ? want : lim;
-    return hash_bin(mode, tier);
+    const int used = want < lim ? want : lim;
+    *cap_lg_out = used;
+    return hash_bin(mode, tier, used > CAPC_LG ? 1 : 0);
 }
 
 // One warp per row.  Computes row_flops, 1P complement bounds, bin + table size.

@@ -234,8 +234,8 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             CU(cudaGetLastError());
             continue;
         }
-        if (b >= BIN_HASH0 && b < BIN_HASH0 + 12) {
-            int mode = (b - BIN_HASH0) / 4, tier = (b - BIN_HASH0) % 4;
+        if (is_hash_bin(b)) {
+            int mode = hash_bin_mode(b), tier = hash_bin_tier(b);
             int kind = numeric ? h->kind : 0;
             int gw = 1;
             HashKernel kern = pick_hash(kind, mode, tier, numeric, &gw);
@@ -246,7 +246,8 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             size_t ebytes = kind == 0 ? 8 : 16;
             size_t table = ((size_t)1 << cap_lg) * ebytes;
             size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
-            size_t smem = (smem_table ? groups * table : 0) + groups * batch;
+            size_t queue = kind == 2 ? 0 : (size_t)64 * (kind == 1 ? 24 : 8);
+            size_t smem = (smem_table ? groups * table : 0) + groups * batch + (threads / 32) * queue;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "hash tier table exceeds shared memory");
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;

@@ -37,6 +37,12 @@ __host__ __device__ constexpr size_t batch_bytes() {
     return KIND == 2 ? 0 : (size_t)GW * 32 * ((KIND == 1 ? 16 : 8) + 4);
 }
 
+// Per-warp deferred-probe queue (WarpProber): 64 entries of (j, slot[, s, a]).
+template <int KIND>
+__host__ __device__ constexpr size_t queue_bytes() {
+    return KIND == 2 ? 0 : (size_t)64 * (KIND == 1 ? 24 : 8);
+}
+
 // Pointers into one group's table region.
 template <int KIND>
 struct Table {
@@ -165,6 +171,106 @@ __device__ __forceinline__ void hash_accumulate(Table<KIND>& tb, int h, long lon
     }
 }
 
+// Warp-level prober for the plain mask: every lane probes its product's
+// first slot; hits accumulate at once, misses on an EMPTY slot are dropped,
+// and the few products whose first slot holds another key are queued in
+// shared memory and resolved 32 at a time.  A linear-probe continuation is
+// rare per product but almost certain somewhere in a warp of 32, so deferring
+// it keeps the common path branch-light and the continuation loop dense.
+// Complement modes (insertion) use the direct per-lane path.
+template <int KIND, int MODE, bool NUMERIC>
+struct WarpProber {
+    Table<KIND> tb;
+    int lg;
+    uint32_t cmask;
+    const int32_t* mrow;
+    int64_t nm;
+    const void* b_val;
+    int32_t* qj;
+    int32_t* qh;
+    long long* qs;
+    long long* qa;
+    int qn;
+    int lane;
+    unsigned long long evaluated;
+
+    __device__ __forceinline__ void hit(int h, long long a, long long s) {
+        evaluated++;
+        hash_accumulate<KIND, NUMERIC>(tb, h, a, b_val, s);
+    }
+
+    __device__ __forceinline__ void flush(int c) {
+        const int base = qn - c;
+        bool act = lane < c;
+        int32_t j = 0;
+        uint32_t h = 0;
+        long long s = 0, a = 0;
+        if (act) {
+            j = qj[base + lane];
+            h = (uint32_t)qh[base + lane];
+            if (KIND == 1) {
+                s = qs[base + lane];
+                a = qa[base + lane];
+            }
+        }
+        __syncwarp();
+        qn = base;
+        while (act) {
+            const int32_t k = tb.keys[h];
+            if (k == j) {
+                hit((int)h, a, s);
+                break;
+            }
+            if (k == EMPTY_KEY) break;
+            h = (h + 1) & cmask;
+        }
+        __syncwarp();
+    }
+
+    // Called by all 32 lanes; `valid` marks lanes that carry a product.
+    __device__ __forceinline__ void put(bool valid, int32_t j, long long a, long long s) {
+        if (MODE != MODE_PLAIN) {
+            if (valid) {
+                const int h = hash_locate_t<MODE, KIND>(tb, j, lg, cmask, mrow, nm);
+                if (h >= 0) hit(h, a, s);
+            }
+            return;
+        }
+        uint32_t h = 0;
+        bool pend = false;
+        if (valid) {
+            h = fib_hash(j, lg);
+            const int32_t k = tb.keys[h];
+            if (k == j) hit((int)h, a, s);
+            else pend = k != EMPTY_KEY;
+        }
+        const unsigned pm = __ballot_sync(FULL, pend);
+        if (pm) {
+            const int pos = qn + __popc(pm & lanemask_lt());
+            if (pend) {
+                qj[pos] = j;
+                qh[pos] = (int32_t)((h + 1) & cmask);
+                if (KIND == 1) {
+                    qs[pos] = s;
+                    qa[pos] = a;
+                }
+            }
+            qn += __popc(pm);
+            if (qn >= 32) {
+                __syncwarp();
+                flush(32);
+            }
+        }
+    }
+
+    __device__ __forceinline__ void drain() {
+        if (qn) {
+            __syncwarp();
+            flush(qn);
+        }
+    }
+};
+
 // ---------------------------------------------------------------------------
 // The row processor.
 // ---------------------------------------------------------------------------
@@ -172,7 +278,7 @@ template <int GW, int KIND, int MODE, bool NUMERIC>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, int64_t i,
                                          int cap_lg, int gt, int bar_id, int* s_warp,
                                          int32_t* bs_incl, long long* bs_base, long long* bs_av,
-                                         unsigned long long& evaluated) {
+                                         unsigned char* wq, unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
     const int lane = gt & 31;
     const int wg = gt >> 5;
@@ -263,6 +369,20 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         constexpr int CH = 32 * U;
         constexpr int NB = GT;
         const int lane32 = gt & 31;
+        WarpProber<KIND, MODE, NUMERIC> pr;
+        pr.tb = tb;
+        pr.lg = cap_lg;
+        pr.cmask = cmask;
+        pr.mrow = p.m_idx + ms;
+        pr.nm = me - ms;
+        pr.b_val = p.b_val;
+        pr.qj = (int32_t*)wq;
+        pr.qh = pr.qj + 64;
+        pr.qs = (long long*)(pr.qh + 64);
+        pr.qa = pr.qs + 64;
+        pr.qn = 0;
+        pr.lane = lane32;
+        pr.evaluated = 0;
         for (int64_t tb0 = as; tb0 < ae; tb0 += NB) {
             const int64_t t = tb0 + gt;
             long long base = 0, av = 0;
@@ -332,14 +452,8 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
                             jj[u] = o < n0 ? __ldg(p.b_idx + b0 + o) : EMPTY_KEY;
                         }
 #pragma unroll
-                        for (int u = 0; u < U; u++) {
-                            if (jj[u] == EMPTY_KEY) continue;
-                            const int h = hash_locate_t<MODE, KIND>(tb, jj[u], cap_lg, cmask,
-                                                                    p.m_idx + ms, me - ms);
-                            if (h < 0) continue;
-                            evaluated++;
-                            hash_accumulate<KIND, NUMERIC>(tb, h, a0, p.b_val, b0 + c + 32 * u + lane32);
-                        }
+                        for (int u = 0; u < U; u++)
+                            pr.put(jj[u] != EMPTY_KEY, jj[u], a0, b0 + c + 32 * u + lane32);
                     }
                 }
                 const int slen = plen < 32 ? plen : 0;
@@ -358,19 +472,14 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
                         jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
                     }
 #pragma unroll
-                    for (int u = 0; u < 2; u++) {
-                        if (jj[u] == EMPTY_KEY) continue;
-                        const int h = hash_locate_t<MODE, KIND>(tb, jj[u], cap_lg, cmask,
-                                                                p.m_idx + ms, me - ms);
-                        if (h < 0) continue;
-                        evaluated++;
-                        hash_accumulate<KIND, NUMERIC>(tb, h, aa[u], p.b_val, ss[u]);
-                    }
+                    for (int u = 0; u < 2; u++) pr.put(jj[u] != EMPTY_KEY, jj[u], aa[u], ss[u]);
                 }
                 if (GW == 1) break;
             }
+            pr.drain();
             if (GW > 1) group_bar(bar_id, GT);
         }
+        evaluated += pr.evaluated;
     }
     group_bar(bar_id, GT);
 
@@ -498,6 +607,8 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
     long long* bs_base = (long long*)bbase;
     long long* bs_av = bs_base + GT;
     int32_t* bs_incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    unsigned char* wq = smem + (SMEM ? (size_t)groups * cap_max * HashEntry<KIND>::bytes : 0) +
+                        (size_t)groups * BATCH_BYTES + (size_t)(threadIdx.x >> 5) * queue_bytes<KIND>();
     Table<KIND> tb;
     tb.bind(base, cap_max);
     unsigned long long evaluated = 0;
@@ -509,7 +620,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
         if (r >= wk.count) break;
         int64_t i = wk.rows[r];
         hash_row<GW, KIND, MODE, NUMERIC>(p, o, tb, i, row_cap_lg[i], gt, bar_id,
-                                          s_warp + g * GW, bs_incl, bs_base, bs_av, evaluated);
+                                          s_warp + g * GW, bs_incl, bs_base, bs_av, wq, evaluated);
     }
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);
