@@ -171,16 +171,65 @@ __device__ __forceinline__ void hash_accumulate(Table<KIND>& tb, int h, long lon
     }
 }
 
-// Warp-level prober for the plain mask: every lane probes its product's
-// first slot; hits accumulate at once, misses on an EMPTY slot are dropped,
-// and the few products whose first slot holds another key are queued in
-// shared memory and resolved 32 at a time.  A linear-probe continuation is
-// rare per product but almost certain somewhere in a warp of 32, so deferring
-// it keeps the common path branch-light and the continuation loop dense.
-// Complement modes (insertion) use the direct per-lane path.
-template <int KIND, int MODE, bool NUMERIC>
+// Table access for the plain-mask prober.  Shared-memory tables are addressed
+// with 32-bit shared-window addresses (ld/red.shared), so the hot loop carries
+// no generic-to-shared conversions; tier-3 tables live in global memory.
+template <bool SMEM>
+struct TabIO;
+
+template <>
+struct TabIO<true> {
+    uint32_t keys, cnt, val;
+    __device__ __forceinline__ void bind(const int32_t* k, int32_t* c, unsigned long long* v) {
+        keys = (uint32_t)__cvta_generic_to_shared(k);
+        cnt = (uint32_t)__cvta_generic_to_shared(c);
+        val = v ? (uint32_t)__cvta_generic_to_shared(v) : 0u;
+    }
+    __device__ __forceinline__ int32_t key(uint32_t h) const {
+        int32_t x;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x) : "r"(keys + (h << 2)));
+        return x;
+    }
+    __device__ __forceinline__ void inc(uint32_t h) const {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cnt + (h << 2)) : "memory");
+    }
+    __device__ __forceinline__ void set(uint32_t h) const {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(cnt + (h << 2)), "r"(1) : "memory");
+    }
+    __device__ __forceinline__ void add64(uint32_t h, unsigned long long x) const {
+        asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(val + (h << 3)), "l"(x) : "memory");
+    }
+};
+
+template <>
+struct TabIO<false> {
+    const int32_t* keys;
+    int32_t* cnt;
+    unsigned long long* val;
+    __device__ __forceinline__ void bind(const int32_t* k, int32_t* c, unsigned long long* v) {
+        keys = k;
+        cnt = c;
+        val = v;
+    }
+    __device__ __forceinline__ int32_t key(uint32_t h) const {
+        return *(volatile const int32_t*)(keys + h);
+    }
+    __device__ __forceinline__ void inc(uint32_t h) const { atomicAdd(cnt + h, 1); }
+    __device__ __forceinline__ void set(uint32_t h) const { cnt[h] = 1; }
+    __device__ __forceinline__ void add64(uint32_t h, unsigned long long x) const { atomicAdd(val + h, x); }
+};
+
+// Warp-level prober for the plain mask: every lane probes its product's first
+// slot; hits accumulate at once, misses on an EMPTY slot are dropped, and the
+// products whose first slot holds another key are queued in shared memory and
+// resolved 32 at a time.  A probe continuation is rare per product but almost
+// certain somewhere in a warp of 32, so deferring it keeps the common path
+// branch-free and the continuation loop dense.  Complement modes (which insert)
+// use the direct per-lane path.
+template <int KIND, int MODE, bool NUMERIC, bool SMEM>
 struct WarpProber {
     Table<KIND> tb;
+    TabIO<SMEM> io;
     int lg;
     uint32_t cmask;
     const int32_t* mrow;
@@ -192,11 +241,19 @@ struct WarpProber {
     long long* qa;
     int qn;
     int lane;
-    unsigned long long evaluated;
+    unsigned evaluated;
 
-    __device__ __forceinline__ void hit(int h, long long a, long long s) {
-        evaluated++;
-        hash_accumulate<KIND, NUMERIC>(tb, h, a, b_val, s);
+    __device__ __forceinline__ void accumulate(uint32_t h, long long a, long long s) {
+        if (KIND == 0) {
+            if (NUMERIC) io.inc(h);
+            else io.set(h);
+        } else {
+            if (NUMERIC) {
+                const long long prod = a * ((const long long*)b_val)[s];
+                io.add64(h, (unsigned long long)prod);
+            }
+            io.set(h);
+        }
     }
 
     __device__ __forceinline__ void flush(int c) {
@@ -216,9 +273,10 @@ struct WarpProber {
         __syncwarp();
         qn = base;
         while (act) {
-            const int32_t k = tb.keys[h];
+            const int32_t k = io.key(h);
             if (k == j) {
-                hit((int)h, a, s);
+                evaluated++;
+                accumulate(h, a, s);
                 break;
             }
             if (k == EMPTY_KEY) break;
@@ -227,27 +285,31 @@ struct WarpProber {
         __syncwarp();
     }
 
-    // Called by all 32 lanes; `valid` marks lanes that carry a product.
-    __device__ __forceinline__ void put(bool valid, int32_t j, long long a, long long s) {
+    // Called by all 32 lanes; lanes without a product pass j = EMPTY_KEY.
+    __device__ __forceinline__ void put(int32_t j, long long a, long long s) {
+        const bool valid = j != EMPTY_KEY;
         if (MODE != MODE_PLAIN) {
             if (valid) {
                 const int h = hash_locate_t<MODE, KIND>(tb, j, lg, cmask, mrow, nm);
-                if (h >= 0) hit(h, a, s);
+                if (h >= 0) {
+                    evaluated++;
+                    accumulate((uint32_t)h, a, s);
+                }
             }
             return;
         }
-        uint32_t h = 0;
-        bool pend = false;
-        if (valid) {
-            h = fib_hash(j, lg);
-            const int32_t k = tb.keys[h];
-            if (k == j) hit((int)h, a, s);
-            else pend = k != EMPTY_KEY;
+        const uint32_t h = fib_hash(j, lg);
+        const int32_t k = io.key(h);
+        const bool hit = valid && k == j;
+        const bool pend = valid && k != j && k != EMPTY_KEY;
+        if (hit) {
+            evaluated++;
+            accumulate(h, a, s);
         }
         const unsigned pm = __ballot_sync(FULL, pend);
         if (pm) {
-            const int pos = qn + __popc(pm & lanemask_lt());
             if (pend) {
+                const int pos = qn + __popc(pm & lanemask_lt());
                 qj[pos] = j;
                 qh[pos] = (int32_t)((h + 1) & cmask);
                 if (KIND == 1) {
@@ -274,7 +336,7 @@ struct WarpProber {
 // ---------------------------------------------------------------------------
 // The row processor.
 // ---------------------------------------------------------------------------
-template <int GW, int KIND, int MODE, bool NUMERIC>
+template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, int64_t i,
                                          int cap_lg, int gt, int bar_id, int* s_warp,
                                          int32_t* bs_incl, long long* bs_base, long long* bs_av,
@@ -369,8 +431,9 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         constexpr int CH = 32 * U;
         constexpr int NB = GT;
         const int lane32 = gt & 31;
-        WarpProber<KIND, MODE, NUMERIC> pr;
+        WarpProber<KIND, MODE, NUMERIC, SMEM> pr;
         pr.tb = tb;
+        pr.io.bind(tb.keys, tb.cnt, tb.val);
         pr.lg = cap_lg;
         pr.cmask = cmask;
         pr.mrow = p.m_idx + ms;
@@ -453,7 +516,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
                         }
 #pragma unroll
                         for (int u = 0; u < U; u++)
-                            pr.put(jj[u] != EMPTY_KEY, jj[u], a0, b0 + c + 32 * u + lane32);
+                            pr.put(jj[u], a0, b0 + c + 32 * u + lane32);
                     }
                 }
                 const int slen = plen < 32 ? plen : 0;
@@ -472,7 +535,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
                         jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
                     }
 #pragma unroll
-                    for (int u = 0; u < 2; u++) pr.put(jj[u] != EMPTY_KEY, jj[u], aa[u], ss[u]);
+                    for (int u = 0; u < 2; u++) pr.put(jj[u], aa[u], ss[u]);
                 }
                 if (GW == 1) break;
             }
@@ -619,7 +682,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
         group_bar(bar_id, GT);
         if (r >= wk.count) break;
         int64_t i = wk.rows[r];
-        hash_row<GW, KIND, MODE, NUMERIC>(p, o, tb, i, row_cap_lg[i], gt, bar_id,
+        hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, i, row_cap_lg[i], gt, bar_id,
                                           s_warp + g * GW, bs_incl, bs_base, bs_av, wq, evaluated);
     }
     if (NUMERIC) {
