@@ -64,6 +64,10 @@ struct Summary {
 };
 
 struct AnalyzeParams {
+    long long tier_flops0;   // rows with <= this many products: 1-warp tier
+    long long tier_flops1;   // ... 4-warp tier; above: 16-warp tier
+    int capc_lg;             // table-size class boundary (log2 slots)
+    int load_shift;          // preferred table size = keys << load_shift
     int family;      // Family
     int comp;        // complemented mask
     int ordered;     // fp64 plus-times: single-warp ordered accumulation
@@ -116,7 +120,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     }
     int need = ceil_log2_i64(2 * keys);
     if (need < 5) need = 5;
-    int want = ceil_log2_i64(4 * keys);
+    int want = ceil_log2_i64(keys << ap.load_shift);
     if (want < 5) want = 5;
     int tier;
     if (ap.ordered) {
@@ -126,13 +130,13 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         for (int t = 0; t < 3; t++) {
             if (need <= tier_cap_lg(ap.pair, t)) { tc = t; break; }
         }
-        int tf = flops <= TIER_FLOPS0 ? 0 : (flops <= TIER_FLOPS1 ? 1 : 2);
+        int tf = flops <= ap.tier_flops0 ? 0 : (flops <= ap.tier_flops1 ? 1 : 2);
         tier = tc > tf ? tc : tf;
     }
     int lim = tier_cap_lg(ap.pair, tier);
     const int used = want < lim ? want : lim;
     *cap_lg_out = used;
-    return hash_bin(mode, tier, used > CAPC_LG ? 1 : 0);
+    return hash_bin(mode, tier, used > ap.capc_lg ? 1 : 0);
 }
 
 // One warp per row.  Computes row_flops, 1P complement bounds, bin + table size.

@@ -77,6 +77,9 @@ struct mm_handle {
     int bin_off[NBINS + 1] = {0};
     Summary sum{};
     mm_stats_t stats{};
+    // ---- tuning (mm_set_tuning) ----
+    long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;
+    int capc_lg = CAPC_LG, load_shift = 2;
     // ---- profiling ----
     bool prof = false;
     cudaEvent_t ev[6] = {};
@@ -312,6 +315,10 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
         case MM_ALGO_AUTO: ap.family = FAM_AUTO; break;
         default: ap.family = FAM_HASH; break;   // msa/mca/heap: see classify_row
     }
+    ap.tier_flops0 = h->tier_flops0;
+    ap.tier_flops1 = h->tier_flops1;
+    ap.capc_lg = h->capc_lg;
+    ap.load_shift = h->load_shift;
     ap.comp = comp;
     ap.ordered = h->kind == 2;
     ap.pair = pair;
@@ -557,6 +564,15 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches) {
         CU(cudaEventElapsedTime(&t, h->ev[from[q]], h->ev[to[q]]));
         ms[q] = t;
     }
+    return MM_OK;
+}
+
+int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
+    if (!h) return fail(MM_ERR_INPUT, "null handle");
+    if (n > 0 && params[0] > 0) h->tier_flops0 = params[0];
+    if (n > 1 && params[1] > 0) h->tier_flops1 = params[1];
+    if (n > 2 && params[2] > 0) h->capc_lg = (int)params[2];
+    if (n > 3 && params[3] > 0 && params[3] <= 4) h->load_shift = (int)params[3];
     return MM_OK;
 }
 
