@@ -135,7 +135,9 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
 /* Kernel-tier tuning of this handle (0 keeps a value): params[0] = max
  * products of a row in the 1-warp tier (default 4096), params[1] = max in the
  * 4-warp tier (65536), params[2] = log2 table-size class boundary (9),
- * params[3] = preferred table size as keys << params[3] (2, i.e. load 1/4). */
+ * params[3] = preferred table size as keys << params[3] (2, i.e. load 1/4),
+ * params[4..6] = shared bytes per row allowed for the MSA / MCA rank-slot
+ * accumulators in the 1-, 4- and 16-warp tiers (6144, 24576, 49152). */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

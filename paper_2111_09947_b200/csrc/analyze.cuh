@@ -26,11 +26,14 @@ enum Bin : int {
     BIN_EMPTY = 0,
     BIN_HASH0 = 1,    // + mode*7 + (tier < 3 ? tier*2 + class : 6)
     BIN_PULL = 22,
-    BIN_MSA = 23,
-    BIN_MCA = 24,
-    BIN_HEAP = 25,
-    NBINS = 26
+    BIN_MSA0 = 23,    // + tier (0..3)
+    BIN_MCA0 = 27,    // + tier
+    BIN_HEAP0 = 31,   // + tier
+    NBINS = 35
 };
+__host__ __device__ constexpr bool is_msa_bin(int b) { return b >= BIN_MSA0 && b < BIN_MSA0 + 4; }
+__host__ __device__ constexpr bool is_mca_bin(int b) { return b >= BIN_MCA0 && b < BIN_MCA0 + 4; }
+__host__ __device__ constexpr bool is_heap_bin(int b) { return b >= BIN_HEAP0 && b < BIN_HEAP0 + 4; }
 
 __host__ __device__ constexpr int hash_bin(int mode, int tier, int cls) {
     return BIN_HASH0 + mode * 7 + (tier < 3 ? tier * 2 + cls : 6);
@@ -57,6 +60,8 @@ struct Summary {
     unsigned long long bin_flops[NBINS];
     int bin_count[NBINS];
     int bin_cap_lg[NBINS];
+    int bin_words[NBINS];    // MSA: largest mask window (32-column words) in the bin
+    int bin_nmmax[NBINS];    // MSA / MCA / heap: largest mask row in the bin
     int max_na;
     int max_nm;
     int flag;
@@ -68,6 +73,7 @@ struct AnalyzeParams {
     long long tier_flops1;   // ... 4-warp tier; above: 16-warp tier
     int capc_lg;             // table-size class boundary (log2 slots)
     int load_shift;          // preferred table size = keys << load_shift
+    int rank_budget[3];      // MSA / MCA shared bytes per group allowed in tiers 0..2
     int family;      // Family
     int comp;        // complemented mask
     int ordered;     // fp64 plus-times: single-warp ordered accumulation
@@ -80,26 +86,44 @@ __device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
     return pair ? tier_cap_lg_pair(tier) : tier_cap_lg_val(tier);
 }
 
+// Shared-memory bytes per row of the rank-slot accumulators.
+__host__ __device__ constexpr int64_t msa_bytes(int64_t words, int64_t nm, int kind) {
+    return 8 * words + (kind == 0 ? 4 : 12) * nm;
+}
+__host__ __device__ constexpr int64_t mca_bytes(int64_t nm, int kind) {
+    return (kind == 0 ? 8 : 16) * nm;
+}
+
 // Chooses the bin for a row and the table size (log2) the row will use.
+// words = 32-column words spanned by the mask row (MSA window).
 __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na, int64_t nm,
                                             int64_t flops, int64_t ncols, int64_t pull_cols,
-                                            int* cap_lg_out) {
+                                            int64_t words, int* cap_lg_out) {
     *cap_lg_out = 0;
     if (flops == 0 || (!ap.comp && nm == 0)) return BIN_EMPTY;
+    const int kind = ap.pair ? 0 : (ap.ordered ? 2 : 1);
+    const int tf = flops <= ap.tier_flops0 ? 0 : (flops <= ap.tier_flops1 ? 1 : 2);
+    const int tr = ap.ordered ? 0 : tf;        // ordered float64 runs one warp per row
     int fam = ap.family;
     if (fam == FAM_AUTO) {
         fam = FAM_HASH;
-        if (!ap.comp && ap.has_bt) {
+        if (!ap.comp) {
             // per-row byte cost model: push vs pull
             int64_t w = 4 + ap.vbytes;
             int64_t push = 16 * na + flops * w;
             int64_t pull = 16 * nm + (nm * na + pull_cols) * w;
-            if (pull < push) fam = FAM_PULL;
+            if (ap.has_bt && pull < push) fam = FAM_PULL;
+            // push: the bitmap accumulator when the mask window is compact
+            else if (msa_bytes(words, nm, kind) <= ap.rank_budget[tr]) fam = FAM_MSA;
         }
     }
     if (fam == FAM_PULL) return BIN_PULL;
-    // MSA / MCA / heap families are routed through their own bins when the
-    // kernels exist; until then they share the hash tiers (same results).
+    if (!ap.comp && (fam == FAM_MSA || fam == FAM_MCA)) {
+        const int64_t bytes = fam == FAM_MSA ? msa_bytes(words, nm, kind) : mca_bytes(nm, kind);
+        const int tier = bytes <= ap.rank_budget[tr] ? tr : 3;
+        return (fam == FAM_MSA ? BIN_MSA0 : BIN_MCA0) + tier;
+    }
+    // hash family (and the complement forms of MSA / heap)
     int64_t fc = flops < ncols ? flops : ncols;
     int mode;
     int64_t keys;
@@ -130,7 +154,6 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         for (int t = 0; t < 3; t++) {
             if (need <= tier_cap_lg(ap.pair, t)) { tc = t; break; }
         }
-        int tf = flops <= ap.tier_flops0 ? 0 : (flops <= ap.tier_flops1 ? 1 : 2);
         tier = tc > tf ? tc : tf;
     }
     int lim = tier_cap_lg(ap.pair, tier);
@@ -146,9 +169,10 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
     __shared__ int s_count[NBINS];
     __shared__ int s_cap[NBINS];
     __shared__ unsigned long long s_bflops[NBINS];
+    __shared__ int s_words[NBINS], s_nmx[NBINS];
     __shared__ unsigned long long s_flops, s_bound;
     __shared__ int s_na, s_nm;
-    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) { s_count[b] = 0; s_cap[b] = 0; s_bflops[b] = 0; }
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) { s_count[b] = 0; s_cap[b] = 0; s_bflops[b] = 0; s_words[b] = 0; s_nmx[b] = 0; }
     if (threadIdx.x == 0) { s_flops = 0; s_bound = 0; s_na = 0; s_nm = 0; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -182,7 +206,10 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
                 my_bound += bd;
             }
             int cap_lg;
-            int b = classify_row(ap, na, nm, f, p.ncols, pull_cols, &cap_lg);
+            int64_t words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
+            int b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg);
+            atomicMax(&s_words[b], (int)(words < 0x7fffffff ? words : 0x7fffffff));
+            atomicMax(&s_nmx[b], (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
             row_bin[i] = (uint8_t)b;
             row_cap_lg[i] = (int8_t)cap_lg;
             atomicAdd(&s_count[b], 1);
@@ -203,6 +230,8 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
             atomicAdd(&s->bin_count[b], s_count[b]);
             atomicAdd(&s->bin_flops[b], s_bflops[b]);
             atomicMax(&s->bin_cap_lg[b], s_cap[b]);
+            atomicMax(&s->bin_words[b], s_words[b]);
+            atomicMax(&s->bin_nmmax[b], s_nmx[b]);
         }
     }
     if (threadIdx.x == 0) {

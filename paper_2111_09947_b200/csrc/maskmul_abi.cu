@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "pull_inner.cuh"
 #include "push_hash.cuh"
+#include "push_rank.cuh"
 #include "scan_compact.cuh"
 
 using namespace mm;
@@ -80,6 +81,7 @@ struct mm_handle {
     // ---- tuning (mm_set_tuning) ----
     long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;
     int capc_lg = CAPC_LG, load_shift = 2;
+    int rank_budget[3] = {6144, 24576, 49152};
     // ---- profiling ----
     bool prof = false;
     cudaEvent_t ev[6] = {};
@@ -209,6 +211,27 @@ HashKernel pick_hash(int kind, int mode, int tier, bool numeric, int* gw) {
     return pick_hash_mode<MODE_CSRCH>(kind, tier, numeric, gw);
 }
 
+typedef void (*RankKernel)(Prob, Out, Work, int, int, unsigned char*);
+
+template <int KIND, bool MSA, bool NUM>
+RankKernel pick_rank_unordered(int tier, int* gw) {
+    switch (tier) {
+        case 0: *gw = 1; return k_push_rank<1, true, KIND, MSA, NUM>;
+        case 1: *gw = 4; return k_push_rank<4, true, KIND, MSA, NUM>;
+        case 2: *gw = 16; return k_push_rank<16, true, KIND, MSA, NUM>;
+        default: *gw = 32; return k_push_rank<32, false, KIND, MSA, NUM>;
+    }
+}
+
+template <bool MSA>
+RankKernel pick_rank(int kind, int tier, bool numeric, int* gw) {
+    if (!numeric || kind == 0) return numeric ? pick_rank_unordered<0, MSA, true>(tier, gw)
+                                              : pick_rank_unordered<0, MSA, false>(tier, gw);
+    if (kind == 1) return pick_rank_unordered<1, MSA, true>(tier, gw);
+    *gw = 1;
+    return tier == 0 ? k_push_rank<1, true, 2, MSA, true> : k_push_rank<1, false, 2, MSA, true>;
+}
+
 // Launch every non-empty bin.  numeric=false: symbolic counts into out.row_nnz.
 int launch_bins(mm_handle* h, bool numeric, const Out& out) {
     cudaStream_t st = h->stream;
@@ -267,6 +290,37 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             CU(cudaGetLastError());
             continue;
         }
+        if (is_msa_bin(b) || is_mca_bin(b)) {
+            const bool msa = is_msa_bin(b);
+            const int tier = b - (msa ? BIN_MSA0 : BIN_MCA0);
+            const int kind = numeric ? h->kind : 0;
+            int gw = 1;
+            RankKernel kern = msa ? pick_rank<true>(kind, tier, numeric, &gw) : pick_rank<false>(kind, tier, numeric, &gw);
+            const bool smem_region = tier < 3;
+            const int threads = gw == 32 ? 1024 : (gw == 16 ? 512 : 256);
+            const int groups = threads / (32 * gw);
+            const int words_max = std::max(h->sum.bin_words[b], 1);
+            const int nm_max = std::max(h->sum.bin_nmmax[b], 1);
+            size_t rb = (size_t)(kind == 0 ? 0 : 8) * nm_max + 4 * (size_t)nm_max +
+                        (msa ? 8 * (size_t)words_max : 4 * (size_t)nm_max);
+            rb = (rb + 15) & ~(size_t)15;
+            const size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            const size_t smem = (smem_region ? groups * rb : 0) + groups * batch;
+            if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "rank tier region exceeds shared memory");
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            const int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
+            unsigned char* gslab = nullptr;
+            if (!smem_region) {
+                CU(cudaMallocAsync((void**)&gslab, (size_t)grid * groups * rb, st));
+                h->allocs.push_back(gslab);
+            }
+            ++g_launches;
+            kern<<<grid, threads, smem, st>>>(h->prob, out, wk, words_max, nm_max, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
         return fail(MM_ERR_INTERNAL, "unhandled bin " + std::to_string(b));
     }
     return MM_OK;
@@ -313,12 +367,15 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     switch (plan->algorithm) {
         case MM_ALGO_INNER: ap.family = FAM_PULL; break;
         case MM_ALGO_AUTO: ap.family = FAM_AUTO; break;
-        default: ap.family = FAM_HASH; break;   // msa/mca/heap: see classify_row
+        case MM_ALGO_MSA: ap.family = FAM_MSA; break;
+        case MM_ALGO_MCA: ap.family = FAM_MCA; break;
+        default: ap.family = FAM_HASH; break;   // hash; heap forms: see classify_row
     }
     ap.tier_flops0 = h->tier_flops0;
     ap.tier_flops1 = h->tier_flops1;
     ap.capc_lg = h->capc_lg;
     ap.load_shift = h->load_shift;
+    for (int t = 0; t < 3; t++) ap.rank_budget[t] = h->rank_budget[t];
     ap.comp = comp;
     ap.ordered = h->kind == 2;
     ap.pair = pair;
@@ -573,6 +630,8 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 1 && params[1] > 0) h->tier_flops1 = params[1];
     if (n > 2 && params[2] > 0) h->capc_lg = (int)params[2];
     if (n > 3 && params[3] > 0 && params[3] <= 4) h->load_shift = (int)params[3];
+    for (int t = 0; t < 3; t++)
+        if (n > 4 + t && params[4 + t] > 0) h->rank_budget[t] = (int)params[4 + t];
     return MM_OK;
 }
 

@@ -1,0 +1,236 @@
+// Product enumeration of one output row, shared by every push accumulator.
+//
+// Row-wise Gustavson (the reference's outer loops, e.g. _kernels.py:48-51):
+// for t in A_i, for s in B_{a_idx[t]}: product (j = b_idx[s], a_val[t]*b_val[s]).
+// The accumulator policy (hash table, windowed bitmap, rank search) only sees
+// `put(j, a, s)` calls; this header decides how the product space is spread
+// over the lanes of a group of GW warps.
+#pragma once
+#include "common.cuh"
+
+namespace mm {
+
+// Group-wide exclusive prefix count of `flag`; returns the prefix, writes the
+// group total to *total.  Uses s_warp[GW] scratch for GW > 1.
+template <int GW>
+__device__ __forceinline__ int group_prefix(bool flag, int* total, int* s_warp, int bar_id, int gt) {
+    unsigned bal = __ballot_sync(FULL, flag);
+    int lane = gt & 31;
+    int in_warp = __popc(bal & lanemask_lt());
+    if (GW == 1) {
+        *total = __popc(bal);
+        return in_warp;
+    } else {
+        int w = gt >> 5;
+        if (lane == 0) s_warp[w] = __popc(bal);
+        group_bar(bar_id, GW * 32);
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < GW; q++) {
+            int c = s_warp[q];
+            if (q < w) before += c;
+            tot += c;
+        }
+        group_bar(bar_id, GW * 32);
+        *total = tot;
+        return before + in_warp;
+    }
+}
+
+// Group-wide inclusive scan of an int (one value per thread); *total = sum.
+template <int GW>
+__device__ __forceinline__ int group_incl_scan(int v, int* total, int* s_warp, int bar_id, int gt) {
+    const int lane = gt & 31;
+    int x = warp_incl_scan(v, lane);
+    if (GW == 1) {
+        *total = __shfl_sync(FULL, x, 31);
+        return x;
+    } else {
+        const int w = gt >> 5;
+        if (lane == 31) s_warp[w] = x;
+        group_bar(bar_id, GW * 32);
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < GW; q++) {
+            const int c = s_warp[q];
+            if (q < w) before += c;
+            tot += c;
+        }
+        group_bar(bar_id, GW * 32);
+        *total = tot;
+        return x + before;
+    }
+}
+
+// Shared-memory staging of one batch of A entries: base of the B row (made
+// relative to the batch's product index), A value (int64 plus-times), and
+// the inclusive product end.  Bytes per group.
+template <int GW, int KIND>
+__host__ __device__ constexpr size_t batch_bytes() {
+    return KIND == 2 ? 0 : (size_t)GW * 32 * ((KIND == 1 ? 16 : 8) + 4);
+}
+
+struct BatchSmem {
+    int32_t* incl;
+    long long* base;
+    long long* av;
+};
+
+// Order-free accumulation (plus-pair counts, int64 sums) over the row's
+// flattened product space, batch by batch (NB = GT entries of A_i):
+//   1. thread gt loads A entry tb0+gt (base of its B row, length); a
+//      group-wide scan gives every product q of the batch the B slot
+//      base[l] + q of the entry l with incl[l-1] <= q < incl[l];
+//   2. warp w owns the contiguous product range [w P/GW, (w+1) P/GW)
+//      (equal work per warp) and walks the entries overlapping it,
+//      32 at a time, one per lane:
+//        portions >= 32 products: warp-wide chunks of 32*U loads
+//        (U independent loads in flight per lane), no search;
+//        shorter portions: flattened into 32-wide windows, the owning
+//        lane found by a shuffle binary search.
+//   Every lane calls pr.put(j, a, s) with j = EMPTY_KEY when it has no
+//   product (the policy may use warp collectives).
+template <int GW, int KIND, class PR>
+__device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as, int64_t ae, int gt,
+                                              int bar_id, int* s_warp, BatchSmem bsm) {
+    constexpr int GT = GW * 32;
+    constexpr int U = 4;
+    constexpr int CH = 32 * U;
+    constexpr int NB = GT;
+    const int lane32 = gt & 31;
+    const int wg = gt >> 5;
+    for (int64_t tb0 = as; tb0 < ae; tb0 += NB) {
+        const int64_t t = tb0 + gt;
+        long long base = 0, av = 0;
+        int len = 0;
+        if (t < ae) {
+            const int32_t k = p.a_idx[t];
+            base = p.b_ptr[k];
+            len = (int)(p.b_ptr[k + 1] - base);
+            if (KIND == 1) av = ((const long long*)p.a_val)[t];
+        }
+        int tot;
+        const int incl = group_incl_scan<GW>(len, &tot, s_warp, bar_id, gt);
+        int q_lo = 0, q_hi = tot;
+        int l_lo = 0, l_end = NB;
+        if (GW > 1) {
+            bsm.incl[gt] = incl;
+            bsm.base[gt] = base - (incl - len);
+            if (KIND == 1) bsm.av[gt] = av;
+            group_bar(bar_id, GT);
+            q_lo = (int)(((long long)tot * wg) / GW);
+            q_hi = (int)(((long long)tot * (wg + 1)) / GW);
+            int lo = 0, hi = NB - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (bsm.incl[mid] <= q_lo) lo = mid + 1; else hi = mid;
+            }
+            l_lo = lo;
+            hi = NB - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (bsm.incl[mid] < q_hi) lo = mid + 1; else hi = mid;
+            }
+            l_end = lo + 1;
+        }
+        for (int l0 = l_lo; l0 < l_end && q_lo < q_hi; l0 += 32) {
+            const int l = l0 + lane32;
+            long long sb = 0, sa = 0;
+            int plen = 0;
+            if (GW == 1) {
+                sb = base;
+                plen = len;
+                sa = av;
+            } else if (l < l_end) {
+                const int e_in = bsm.incl[l];
+                const int e_ex = l > 0 ? bsm.incl[l - 1] : 0;
+                const int a0 = e_ex > q_lo ? e_ex : q_lo;
+                const int a1 = e_in < q_hi ? e_in : q_hi;
+                plen = a1 > a0 ? a1 - a0 : 0;
+                sb = bsm.base[l] + a0;
+                if (KIND == 1) sa = bsm.av[l];
+            }
+            unsigned longm = __ballot_sync(FULL, plen >= 32);
+            while (longm) {
+                const int src = __ffs(longm) - 1;
+                longm &= longm - 1;
+                const long long b0 = shfl64(sb, src);
+                const int n0 = __shfl_sync(FULL, plen, src);
+                const long long a0 = KIND == 1 ? __shfl_sync(FULL, sa, src) : 0;
+                const int32_t* bp = p.b_idx + b0;
+                for (int c = 0; c < n0; c += CH) {
+                    int32_t jj[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int o = c + 32 * u + lane32;
+                        jj[u] = o < n0 ? __ldg(bp + o) : EMPTY_KEY;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) pr.put(jj[u], a0, b0 + c + 32 * u + lane32);
+                }
+            }
+            const int slen = plen < 32 ? plen : 0;
+            const int sincl = warp_incl_scan(slen, lane32);
+            const int stot = __shfl_sync(FULL, sincl, 31);
+            const int sexcl = sincl - slen;
+            for (int w0 = 0; w0 < stot; w0 += 64) {
+                int32_t jj[2];
+                long long ss[2], aa[2];
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const int q = w0 + 32 * u + lane32;
+                    const int own = owner_of(sincl, q < stot ? q : stot - 1);
+                    ss[u] = shfl64(sb, own) + (q - __shfl_sync(FULL, sexcl, own));
+                    aa[u] = KIND == 1 ? __shfl_sync(FULL, sa, own) : 0;
+                    jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                }
+#pragma unroll
+                for (int u = 0; u < 2; u++) pr.put(jj[u], aa[u], ss[u]);
+            }
+            if (GW == 1) break;
+        }
+        pr.drain();
+        if (GW > 1) group_bar(bar_id, GT);
+    }
+}
+
+// Ordered float64 accumulation for one warp: A entries in ascending order
+// (= ascending k, the reference's sum order, _kernels.py:48-65), lanes over
+// the entries of B_k; within one k no two lanes share a column, and
+// __syncwarp orders consecutive k, so every slot folds its products exactly
+// like the reference (first product stored, then added: _kernels.py:58-65).
+// loc.locate(j) -> slot or -1 (masked out); loc.fold(slot, prod); loc.mark(slot).
+template <bool NUMERIC, class LOC>
+__device__ __forceinline__ unsigned ordered_products_f64(const Prob& p, LOC& loc, int64_t as, int64_t ae,
+                                                         int lane) {
+    const double* av_p = (const double*)p.a_val;
+    const double* bv_p = (const double*)p.b_val;
+    unsigned evaluated = 0;
+    for (int64_t tb0 = as; tb0 < ae; tb0 += 32) {
+        const int64_t t = tb0 + lane;
+        int64_t bs = 0, be = 0;
+        double av = 0.0;
+        if (t < ae) {
+            const int32_t k = p.a_idx[t];
+            bs = p.b_ptr[k];
+            be = p.b_ptr[k + 1];
+            av = av_p[t];
+        }
+        const int nb = (int)min((int64_t)32, ae - tb0);
+        for (int q = 0; q < nb; q++) {
+            const int64_t s0 = shfl64(bs, q), s1 = shfl64(be, q);
+            const double a = __shfl_sync(FULL, av, q);
+            for (int64_t s = s0 + lane; s < s1; s += 32) {
+                const int h = loc.locate(p.b_idx[s]);
+                if (h < 0) continue;
+                evaluated++;
+                if (NUMERIC) loc.fold(h, a * bv_p[s]);
+                else loc.mark(h);
+            }
+            __syncwarp();
+        }
+    }
+    return evaluated;
+}
+
+}  // namespace mm

@@ -22,6 +22,7 @@
 #pragma once
 #include "analyze.cuh"
 #include "common.cuh"
+#include "product_loop.cuh"
 
 namespace mm {
 
@@ -29,13 +30,6 @@ template <int KIND>
 struct HashEntry {
     static constexpr int bytes = KIND == 0 ? 8 : 16;
 };
-
-// Per-group shared-memory staging of one batch of A entries (order-free kinds):
-// base (8 B) [+ a value (8 B)] + inclusive product end (4 B) per thread.
-template <int GW, int KIND>
-__host__ __device__ constexpr size_t batch_bytes() {
-    return KIND == 2 ? 0 : (size_t)GW * 32 * ((KIND == 1 ? 16 : 8) + 4);
-}
 
 // Per-warp deferred-probe queue (WarpProber): 64 entries of (j, slot[, s, a]).
 template <int KIND>
@@ -85,59 +79,6 @@ __device__ __forceinline__ int probe_insert(int32_t* keys, int32_t j, int lg, ui
             if (old == EMPTY_KEY || old == j) return (int)h;
         }
         h = (h + 1) & mask;
-    }
-}
-
-// Group-wide exclusive prefix count of `flag`; returns the prefix, writes the
-// group total to *total.  Uses s_warp[GW] scratch for GW > 1.
-template <int GW>
-__device__ __forceinline__ int group_prefix(bool flag, int* total, int* s_warp, int bar_id,
-                                            int gt) {
-    unsigned bal = __ballot_sync(FULL, flag);
-    int lane = gt & 31;
-    int in_warp = __popc(bal & lanemask_lt());
-    if (GW == 1) {
-        *total = __popc(bal);
-        return in_warp;
-    } else {
-        int w = gt >> 5;
-        if (lane == 0) s_warp[w] = __popc(bal);
-        group_bar(bar_id, GW * 32);
-        int before = 0, tot = 0;
-#pragma unroll
-        for (int q = 0; q < GW; q++) {
-            int c = s_warp[q];
-            if (q < w) before += c;
-            tot += c;
-        }
-        group_bar(bar_id, GW * 32);
-        *total = tot;
-        return before + in_warp;
-    }
-}
-
-// Group-wide inclusive scan of an int (one value per thread); *total = sum.
-template <int GW>
-__device__ __forceinline__ int group_incl_scan(int v, int* total, int* s_warp, int bar_id, int gt) {
-    const int lane = gt & 31;
-    int x = warp_incl_scan(v, lane);
-    if (GW == 1) {
-        *total = __shfl_sync(FULL, x, 31);
-        return x;
-    } else {
-        const int w = gt >> 5;
-        if (lane == 31) s_warp[w] = x;
-        group_bar(bar_id, GW * 32);
-        int before = 0, tot = 0;
-#pragma unroll
-        for (int q = 0; q < GW; q++) {
-            const int c = s_warp[q];
-            if (q < w) before += c;
-            tot += c;
-        }
-        group_bar(bar_id, GW * 32);
-        *total = tot;
-        return x + before;
     }
 }
 
@@ -333,14 +274,44 @@ struct WarpProber {
     }
 };
 
+// Slot locator for the ordered float64 path (single warp).
+template <int MODE>
+struct HashLocatorF64 {
+    int32_t* keys;
+    int32_t* cnt;
+    double* vals;
+    int lg;
+    uint32_t cmask;
+    const int32_t* mrow;
+    int64_t nm;
+    __device__ __forceinline__ int locate(int32_t j) {
+        if (MODE == MODE_PLAIN) {
+            const int h = probe_find(keys, j, lg, cmask);
+            return h < 0 ? -1 : h;
+        }
+        if (MODE == MODE_CSRCH && contains_sorted(mrow, nm, j)) return -1;
+        const int h = probe_insert(keys, j, lg, cmask);
+        return cnt[h] < 0 ? -1 : h;
+    }
+    __device__ __forceinline__ void fold(int h, double prod) {
+        if (cnt[h] == 0) {
+            vals[h] = prod;
+            cnt[h] = 1;
+        } else {
+            vals[h] += prod;
+        }
+    }
+    __device__ __forceinline__ void mark(int h) { cnt[h] = 1; }
+};
+
 // ---------------------------------------------------------------------------
 // The row processor.
 // ---------------------------------------------------------------------------
 template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, int64_t i,
                                          int cap_lg, int gt, int bar_id, int* s_warp,
-                                         int32_t* bs_incl, long long* bs_base, long long* bs_av,
-                                         unsigned char* wq, unsigned long long& evaluated) {
+                                         BatchSmem bsm, unsigned char* wq,
+                                         unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
     const int lane = gt & 31;
     const int wg = gt >> 5;
@@ -373,64 +344,9 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
 
     // 3. products
     if (KIND == 2) {
-        // ordered float64: one warp (GW == 1), k ascending, lanes over B_k
-        const double* av_p = (const double*)p.a_val;
-        const double* bv_p = (const double*)p.b_val;
-        double* vals = (double*)tb.val;
-        for (int64_t tb0 = as; tb0 < ae; tb0 += 32) {
-            int64_t t = tb0 + lane;
-            int64_t bs = 0, be = 0;
-            double av = 0.0;
-            if (t < ae) {
-                int32_t k = p.a_idx[t];
-                bs = p.b_ptr[k];
-                be = p.b_ptr[k + 1];
-                av = av_p[t];
-            }
-            int nb = (int)min((int64_t)32, ae - tb0);
-            for (int q = 0; q < nb; q++) {
-                int64_t s0 = shfl64(bs, q), s1 = shfl64(be, q);
-                double a = __shfl_sync(FULL, av, q);
-                for (int64_t s = s0 + lane; s < s1; s += 32) {
-                    int32_t j = p.b_idx[s];
-                    int h;
-                    if (MODE == MODE_PLAIN) {
-                        h = probe_find(tb.keys, j, cap_lg, cmask);
-                        if (h < 0) continue;
-                    } else {
-                        if (MODE == MODE_CSRCH && contains_sorted(p.m_idx + ms, me - ms, j)) continue;
-                        h = probe_insert(tb.keys, j, cap_lg, cmask);
-                        if (tb.cnt[h] < 0) continue;
-                    }
-                    evaluated++;
-                    if (NUMERIC) {
-                        double prod = a * bv_p[s];
-                        if (tb.cnt[h] == 0) { vals[h] = prod; tb.cnt[h] = 1; }
-                        else vals[h] += prod;
-                    } else {
-                        tb.cnt[h] = 1;
-                    }
-                }
-                __syncwarp();
-            }
-        }
+        HashLocatorF64<MODE> loc{tb.keys, tb.cnt, (double*)tb.val, cap_lg, cmask, p.m_idx + ms, me - ms};
+        evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
     } else {
-        // Order-free integer accumulation over the row's flattened product
-        // space, batch by batch (NB = GT entries of A_i per batch):
-        //   1. thread gt loads A entry tb0+gt (base of its B row, length); a
-        //      group-wide scan assigns every product q of the batch the B slot
-        //      s_base[l] + q of the entry l with s_incl[l-1] <= q < s_incl[l];
-        //   2. warp w owns the contiguous product range [w P/GW, (w+1) P/GW)
-        //      (equal work per warp) and walks the entries overlapping it,
-        //      32 at a time, one per lane:
-        //        portions >= 32 products: warp-wide chunks of 32*U loads
-        //        (U independent loads in flight per lane), no search;
-        //        shorter portions: flattened into 32-wide windows, the owning
-        //        lane found by a shuffle binary search.
-        constexpr int U = 4;
-        constexpr int CH = 32 * U;
-        constexpr int NB = GT;
-        const int lane32 = gt & 31;
         WarpProber<KIND, MODE, NUMERIC, SMEM> pr;
         pr.tb = tb;
         pr.io.bind(tb.keys, tb.cnt, tb.val);
@@ -444,104 +360,9 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         pr.qs = (long long*)(pr.qh + 64);
         pr.qa = pr.qs + 64;
         pr.qn = 0;
-        pr.lane = lane32;
+        pr.lane = lane;
         pr.evaluated = 0;
-        for (int64_t tb0 = as; tb0 < ae; tb0 += NB) {
-            const int64_t t = tb0 + gt;
-            long long base = 0, av = 0;
-            int len = 0;
-            if (t < ae) {
-                const int32_t k = p.a_idx[t];
-                base = p.b_ptr[k];
-                len = (int)(p.b_ptr[k + 1] - base);
-                if (KIND == 1) av = ((const long long*)p.a_val)[t];
-            }
-            int tot;
-            const int incl = group_incl_scan<GW>(len, &tot, s_warp, bar_id, gt);
-            int q_lo = 0, q_hi = tot;
-            int l_lo = 0, l_end = NB;
-            if (GW > 1) {
-                bs_incl[gt] = incl;
-                bs_base[gt] = base - (incl - len);
-                if (KIND == 1) bs_av[gt] = av;
-                group_bar(bar_id, GT);
-                q_lo = (int)(((long long)tot * wg) / GW);
-                q_hi = (int)(((long long)tot * (wg + 1)) / GW);
-                // entries overlapping [q_lo, q_hi): first with incl > q_lo ...
-                int lo = 0, hi = NB - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (bs_incl[mid] <= q_lo) lo = mid + 1; else hi = mid;
-                }
-                l_lo = lo;
-                // ... through the first with incl >= q_hi
-                hi = NB - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (bs_incl[mid] < q_hi) lo = mid + 1; else hi = mid;
-                }
-                l_end = lo + 1;
-            }
-            for (int l0 = l_lo; l0 < l_end && q_lo < q_hi; l0 += 32) {
-                // this lane's entry and its portion inside [q_lo, q_hi)
-                const int l = l0 + lane32;
-                long long sb = 0, sa = 0;
-                int plen = 0;
-                if (GW == 1) {
-                    sb = base;
-                    plen = len;
-                    sa = av;
-                } else if (l < l_end) {
-                    const int e_in = bs_incl[l];
-                    const int e_ex = l > 0 ? bs_incl[l - 1] : 0;
-                    const int a0 = e_ex > q_lo ? e_ex : q_lo;
-                    const int a1 = e_in < q_hi ? e_in : q_hi;
-                    plen = a1 > a0 ? a1 - a0 : 0;
-                    sb = bs_base[l] + a0;
-                    if (KIND == 1) sa = bs_av[l];
-                }
-                unsigned longm = __ballot_sync(FULL, plen >= 32);
-                while (longm) {
-                    const int src = __ffs(longm) - 1;
-                    longm &= longm - 1;
-                    const long long b0 = shfl64(sb, src);
-                    const int n0 = __shfl_sync(FULL, plen, src);
-                    const long long a0 = KIND == 1 ? __shfl_sync(FULL, sa, src) : 0;
-                    for (int c = 0; c < n0; c += CH) {
-                        int32_t jj[U];
-#pragma unroll
-                        for (int u = 0; u < U; u++) {
-                            const int o = c + 32 * u + lane32;
-                            jj[u] = o < n0 ? __ldg(p.b_idx + b0 + o) : EMPTY_KEY;
-                        }
-#pragma unroll
-                        for (int u = 0; u < U; u++)
-                            pr.put(jj[u], a0, b0 + c + 32 * u + lane32);
-                    }
-                }
-                const int slen = plen < 32 ? plen : 0;
-                const int sincl = warp_incl_scan(slen, lane32);
-                const int stot = __shfl_sync(FULL, sincl, 31);
-                const int sexcl = sincl - slen;
-                for (int w0 = 0; w0 < stot; w0 += 64) {
-                    int32_t jj[2];
-                    long long ss[2], aa[2];
-#pragma unroll
-                    for (int u = 0; u < 2; u++) {
-                        const int q = w0 + 32 * u + lane32;
-                        const int own = owner_of(sincl, q < stot ? q : stot - 1);
-                        ss[u] = shfl64(sb, own) + (q - __shfl_sync(FULL, sexcl, own));
-                        aa[u] = KIND == 1 ? __shfl_sync(FULL, sa, own) : 0;
-                        jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 2; u++) pr.put(jj[u], aa[u], ss[u]);
-                }
-                if (GW == 1) break;
-            }
-            pr.drain();
-            if (GW > 1) group_bar(bar_id, GT);
-        }
+        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
         evaluated += pr.evaluated;
     }
     group_bar(bar_id, GT);
@@ -667,9 +488,10 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
                                              HashEntry<KIND>::bytes;
     unsigned char* bbase = smem + (SMEM ? (size_t)groups * cap_max * HashEntry<KIND>::bytes : 0) +
                            (size_t)g * BATCH_BYTES;
-    long long* bs_base = (long long*)bbase;
-    long long* bs_av = bs_base + GT;
-    int32_t* bs_incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    BatchSmem bsm;
+    bsm.base = (long long*)bbase;
+    bsm.av = bsm.base + GT;
+    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
     unsigned char* wq = smem + (SMEM ? (size_t)groups * cap_max * HashEntry<KIND>::bytes : 0) +
                         (size_t)groups * BATCH_BYTES + (size_t)(threadIdx.x >> 5) * queue_bytes<KIND>();
     Table<KIND> tb;
@@ -683,7 +505,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
         if (r >= wk.count) break;
         int64_t i = wk.rows[r];
         hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, i, row_cap_lg[i], gt, bar_id,
-                                          s_warp + g * GW, bs_incl, bs_base, bs_av, wq, evaluated);
+                                          s_warp + g * GW, bsm, wq, evaluated);
     }
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);

@@ -1,0 +1,251 @@
+// Push path, rank-slot accumulators: MSA (windowed bitmap) and MCA (rank search).
+//
+// Both keep one value slot per mask entry (slot r = the r-th column of M_i),
+// so the output row is produced in mask order without any lookup — the
+// plain-mask gather of the reference (_kernels.py:78-85, 308-313).
+//
+// MSA — reference msa_numeric / msa_symbolic (_kernels.py:30-123): a dense
+// state per column.  GPU form: a bitmap over the mask row's column window
+// [lo, hi] (1 bit per column, 32 columns per word) plus, per word, the mask
+// rank of its first set bit.  A product with column j tests bit j-lo; when set,
+// its slot is prefix[word] + popc(word & below(j)).  One shared load per
+// product, no probing, no divergence but the hit.
+//
+// MCA — reference mca_numeric / mca_symbolic (_kernels.py:275-344): arrays of
+// length nnz(M_i) indexed by mask rank, position found by merging B_k against
+// M_i.  GPU form: the mask row staged in shared memory, the rank of each
+// product found by a branch-free binary search.
+//
+// Plain masks only (MCA rejects complement, multiply.py:67-69; the MSA
+// complement form runs through the hash kernels).
+#pragma once
+#include "analyze.cuh"
+#include "common.cuh"
+#include "product_loop.cuh"
+
+namespace mm {
+
+template <int KIND>
+struct RankSlots {
+    int32_t* cnt;
+    unsigned long long* val;
+};
+
+// One product's accumulation into slot r (order-free kinds).
+template <int KIND, bool NUMERIC>
+__device__ __forceinline__ void rank_accumulate(RankSlots<KIND>& sl, int r, long long a,
+                                                const void* b_val, long long s) {
+    if (KIND == 0) {
+        if (NUMERIC) atomicAdd(sl.cnt + r, 1);
+        else sl.cnt[r] = 1;
+    } else {
+        if (NUMERIC) {
+            const long long prod = a * ((const long long*)b_val)[s];
+            atomicAdd(sl.val + r, (unsigned long long)prod);
+        }
+        sl.cnt[r] = 1;
+    }
+}
+
+// --- MSA bitmap probe ------------------------------------------------------
+struct MsaBits {
+    const uint32_t* bits;
+    const int32_t* pre;
+    int32_t lo;
+    uint32_t span;   // hi - lo
+    // slot of column j, or -1
+    __device__ __forceinline__ int rank(int32_t j) const {
+        const uint32_t off = (uint32_t)(j - lo);
+        if (off > span) return -1;
+        const uint32_t w = off >> 5;
+        const uint32_t word = bits[w];
+        const uint32_t b = off & 31u;
+        if (!((word >> b) & 1u)) return -1;
+        return pre[w] + __popc(word & ((1u << b) - 1u));
+    }
+};
+
+// --- MCA rank search -------------------------------------------------------
+struct McaRow {
+    const int32_t* m;   // mask row (shared)
+    int nm;
+    int steps;          // ceil(log2(nm + 1))
+    __device__ __forceinline__ int rank(int32_t j) const {
+        // branch-free lower bound with a fixed step count
+        int pos = 0;
+        for (int st = steps - 1; st >= 0; st--) {
+            const int q = pos + (1 << st);
+            if (q <= nm && m[q - 1] < j) pos = q;
+        }
+        return (pos < nm && m[pos] == j) ? pos : -1;
+    }
+};
+
+template <int KIND, bool NUMERIC, class R>
+struct RankProber {
+    R r;
+    RankSlots<KIND> sl;
+    const void* b_val;
+    unsigned evaluated;
+    __device__ __forceinline__ void put(int32_t j, long long a, long long s) {
+        if (j == EMPTY_KEY) return;
+        const int k = r.rank(j);
+        if (k >= 0) {
+            evaluated++;
+            rank_accumulate<KIND, NUMERIC>(sl, k, a, b_val, s);
+        }
+    }
+    __device__ __forceinline__ void drain() {}
+};
+
+template <class R>
+struct RankLocatorF64 {
+    R r;
+    int32_t* cnt;
+    double* vals;
+    __device__ __forceinline__ int locate(int32_t j) { return r.rank(j); }
+    __device__ __forceinline__ void fold(int k, double prod) {
+        if (cnt[k] == 0) {
+            vals[k] = prod;
+            cnt[k] = 1;
+        } else {
+            vals[k] += prod;
+        }
+    }
+    __device__ __forceinline__ void mark(int k) { cnt[k] = 1; }
+};
+
+// Per-group region: [val: 8*NM if KIND != 0][cnt: 4*NM][MSA: bits 4*W, pre 4*W | MCA: mask 4*NM]
+template <int KIND>
+__host__ __device__ constexpr size_t rank_region_bytes(bool msa, int64_t words, int64_t nm) {
+    return (size_t)(KIND == 0 ? 0 : 8) * nm + 4 * (size_t)nm + (msa ? 8 * (size_t)words : 4 * (size_t)nm);
+}
+
+template <int GW, int KIND, bool MSA, bool NUMERIC>
+__device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned char* region, int nm_max,
+                                         int64_t i, int gt, int bar_id, int* s_warp, BatchSmem bsm,
+                                         unsigned long long& evaluated) {
+    constexpr int GT = GW * 32;
+    const int lane = gt & 31;
+    const int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1];
+    const int64_t ms = p.m_ptr[i], me = p.m_ptr[i + 1];
+    const int nm = (int)(me - ms);
+    RankSlots<KIND> sl;
+    sl.val = KIND == 0 ? nullptr : (unsigned long long*)region;
+    sl.cnt = (int32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max));
+    unsigned char* aux = (unsigned char*)(sl.cnt + nm_max);
+    const int32_t lo = p.m_idx[ms];
+    const int32_t hi = p.m_idx[me - 1];
+    const int words = ((hi - lo) >> 5) + 1;
+    uint32_t* bits = (uint32_t*)aux;
+    int32_t* pre = (int32_t*)(aux + 4 * (size_t)(MSA ? words : 0));
+    int32_t* mrow = (int32_t*)aux;
+
+    // 1. clear slots (and the bitmap window), 2. mark the mask row
+    for (int r = gt; r < nm; r += GT) {
+        sl.cnt[r] = 0;
+        if (KIND == 1) sl.val[r] = 0ull;
+    }
+    if (MSA)
+        for (int w = gt; w < words; w += GT) bits[w] = 0u;
+    group_bar(bar_id, GT);
+    for (int r = gt; r < nm; r += GT) {
+        const int32_t j = p.m_idx[ms + r];
+        if (MSA) {
+            const uint32_t off = (uint32_t)(j - lo);
+            const uint32_t w = off >> 5;
+            atomicOr(bits + w, 1u << (off & 31u));
+            if (r == 0 || (((uint32_t)(p.m_idx[ms + r - 1] - lo)) >> 5) != w) pre[w] = r;
+        } else {
+            mrow[r] = j;
+        }
+    }
+    group_bar(bar_id, GT);
+
+    // 3. products
+    if (MSA) {
+        MsaBits rb{bits, pre, lo, (uint32_t)(hi - lo)};
+        if (KIND == 2) {
+            RankLocatorF64<MsaBits> loc{rb, sl.cnt, (double*)sl.val};
+            evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+        } else {
+            RankProber<KIND, NUMERIC, MsaBits> pr{rb, sl, p.b_val, 0u};
+            flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+            evaluated += pr.evaluated;
+        }
+    } else {
+        int steps = 0;
+        while ((1 << steps) <= nm) steps++;
+        McaRow rb{mrow, nm, steps};
+        if (KIND == 2) {
+            RankLocatorF64<McaRow> loc{rb, sl.cnt, (double*)sl.val};
+            evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+        } else {
+            RankProber<KIND, NUMERIC, McaRow> pr{rb, sl, p.b_val, 0u};
+            flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+            evaluated += pr.evaluated;
+        }
+    }
+    group_bar(bar_id, GT);
+
+    // 4. gather in mask order
+    const int64_t w0 = NUMERIC ? o.off[i] : 0;
+    int running = 0;
+    for (int base = 0; base < nm; base += GT) {
+        const int r = base + gt;
+        const bool set = r < nm && sl.cnt[r] > 0;
+        int tot;
+        const int pos = group_prefix<GW>(set, &tot, s_warp, bar_id, gt);
+        if (NUMERIC && set) {
+            const int64_t d = w0 + running + pos;
+            o.idx[d] = p.m_idx[ms + r];
+            if (KIND == 0) {
+                if (o.out_f64) ((double*)o.val)[d] = (double)sl.cnt[r];
+                else ((long long*)o.val)[d] = sl.cnt[r];
+            } else {
+                ((unsigned long long*)o.val)[d] = sl.val[r];
+            }
+        }
+        running += tot;
+    }
+    if (gt == 0) o.row_nnz[i] = running;
+    group_bar(bar_id, GT);
+}
+
+// Groups of GW warps fetch rows of one bin.  SMEM: the per-group region lives
+// in dynamic shared memory, otherwise in one global slab per group (tier 3).
+template <int GW, bool SMEM, int KIND, bool MSA, bool NUMERIC>
+__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256))
+k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gslab) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_row[16];
+    __shared__ int s_warp[32];
+    constexpr int GT = GW * 32;
+    const int groups = blockDim.x / GT;
+    const int g = threadIdx.x / GT;
+    const int gt = threadIdx.x % GT;
+    const int bar_id = 1 + g;
+    const size_t rbytes = (rank_region_bytes<KIND>(MSA, words_max, nm_max) + 15) & ~(size_t)15;
+    unsigned char* region = SMEM ? smem + (size_t)g * rbytes : gslab + ((size_t)blockIdx.x * groups + g) * rbytes;
+    unsigned char* bbase = smem + (SMEM ? (size_t)groups * rbytes : 0) + (size_t)g * batch_bytes<GW, KIND>();
+    BatchSmem bsm;
+    bsm.base = (long long*)bbase;
+    bsm.av = bsm.base + GT;
+    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    unsigned long long evaluated = 0;
+    for (;;) {
+        if (gt == 0) s_row[g] = atomicAdd(wk.cursor, 1);
+        group_bar(bar_id, GT);
+        const int r = s_row[g];
+        group_bar(bar_id, GT);
+        if (r >= wk.count) break;
+        rank_row<GW, KIND, MSA, NUMERIC>(p, o, region, nm_max, wk.rows[r], gt, bar_id, s_warp + g * GW, bsm,
+                                         evaluated);
+    }
+    if (NUMERIC) {
+        const long long e = warp_sum_ll((long long)evaluated);
+        if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);
+    }
+}
+
+}  // namespace mm
