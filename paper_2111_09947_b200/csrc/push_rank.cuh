@@ -81,6 +81,64 @@ struct McaRow {
     }
 };
 
+// Branch-free MSA probe for the order-free kinds: every step predicated,
+// 32-bit shared-window addresses, no divergence (the lazy rule holds: the
+// B value of a product is loaded only when its column survives the mask).
+template <int KIND, bool NUMERIC>
+struct MsaProber {
+    uint32_t bits_s, pre_s, cnt_s, val_s;
+    int32_t lo;
+    uint32_t span;
+    const void* b_val;
+    unsigned evaluated;
+    __device__ __forceinline__ void put(int32_t j, long long a, long long s) {
+        const uint32_t off = (uint32_t)(j - lo);     // j = EMPTY_KEY -> off > span
+        uint32_t word = 0, pre = 0, hitbit;
+        const uint32_t w4 = (off >> 5) << 2;
+        asm volatile(
+            "{\n\t.reg .pred pin;\n\t"
+            "setp.le.u32 pin, %1, %2;\n\t"
+            "@pin ld.shared.u32 %0, [%3];\n\t}"
+            : "+r"(word)
+            : "r"(off), "r"(span), "r"(bits_s + w4));
+        const uint32_t b = off & 31u;
+        hitbit = (word >> b) & 1u;
+        asm volatile(
+            "{\n\t.reg .pred ph;\n\t"
+            "setp.ne.u32 ph, %1, 0;\n\t"
+            "@ph ld.shared.u32 %0, [%2];\n\t}"
+            : "+r"(pre)
+            : "r"(hitbit), "r"(pre_s + w4));
+        const uint32_t rank = pre + __popc(word & ((1u << b) - 1u));
+        evaluated += hitbit;
+        if (KIND == 0) {
+            if (NUMERIC)
+                asm volatile(
+                    "{\n\t.reg .pred ph;\n\t"
+                    "setp.ne.u32 ph, %0, 0;\n\t"
+                    "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"(hitbit),
+                    "r"(cnt_s + (rank << 2))
+                    : "memory");
+            else
+                asm volatile(
+                    "{\n\t.reg .pred ph;\n\t"
+                    "setp.ne.u32 ph, %0, 0;\n\t"
+                    "@ph st.shared.u32 [%1], 1;\n\t}" ::"r"(hitbit),
+                    "r"(cnt_s + (rank << 2))
+                    : "memory");
+        } else {
+            if (hitbit) {
+                if (NUMERIC) {
+                    const long long prod = a * ((const long long*)b_val)[s];
+                    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(val_s + (rank << 3)), "l"(prod) : "memory");
+                }
+                asm volatile("st.shared.u32 [%0], 1;" ::"r"(cnt_s + (rank << 2)) : "memory");
+            }
+        }
+    }
+    __device__ __forceinline__ void drain() {}
+};
+
 template <int KIND, bool NUMERIC, class R>
 struct RankProber {
     R r;
@@ -121,7 +179,7 @@ __host__ __device__ constexpr size_t rank_region_bytes(bool msa, int64_t words, 
     return (size_t)(KIND == 0 ? 0 : 8) * nm + 4 * (size_t)nm + (msa ? 8 * (size_t)words : 4 * (size_t)nm);
 }
 
-template <int GW, int KIND, bool MSA, bool NUMERIC>
+template <int GW, int KIND, bool MSA, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned char* region, int nm_max,
                                          int64_t i, int gt, int bar_id, int* s_warp, BatchSmem bsm,
                                          unsigned long long& evaluated) {
@@ -169,9 +227,23 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
             RankLocatorF64<MsaBits> loc{rb, sl.cnt, (double*)sl.val};
             evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
         } else {
+          if (!SMEM) {
             RankProber<KIND, NUMERIC, MsaBits> pr{rb, sl, p.b_val, 0u};
             flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
             evaluated += pr.evaluated;
+          } else {
+            MsaProber<KIND, NUMERIC> pr;
+            pr.bits_s = (uint32_t)__cvta_generic_to_shared(bits);
+            pr.pre_s = (uint32_t)__cvta_generic_to_shared(pre);
+            pr.cnt_s = (uint32_t)__cvta_generic_to_shared(sl.cnt);
+            pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(sl.val);
+            pr.lo = lo;
+            pr.span = (uint32_t)(hi - lo);
+            pr.b_val = p.b_val;
+            pr.evaluated = 0u;
+            flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+            evaluated += pr.evaluated;
+          }
         }
     } else {
         int steps = 0;
@@ -239,7 +311,7 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
         const int r = s_row[g];
         group_bar(bar_id, GT);
         if (r >= wk.count) break;
-        rank_row<GW, KIND, MSA, NUMERIC>(p, o, region, nm_max, wk.rows[r], gt, bar_id, s_warp + g * GW, bsm,
+        rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, wk.rows[r], gt, bar_id, s_warp + g * GW, bsm,
                                          evaluated);
     }
     if (NUMERIC) {

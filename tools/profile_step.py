@@ -14,7 +14,7 @@ from paper_2111_09947_b200.multiply import multiply_device, reduce_sum
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=20)
-ap.add_argument("--algo", default="hash")
+ap.add_argument("--algo", default="auto")
 ap.add_argument("--reps", type=int, default=2)
 args = ap.parse_args()
 low = workloads.triangle_lower(args.scale)
