@@ -160,13 +160,15 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 const int32_t* bp = p.b_idx + b0;
                 for (int c = 0; c < n0; c += CH) {
                     int32_t jj[U];
+                    long long aa[U], ss[U];
 #pragma unroll
                     for (int u = 0; u < U; u++) {
                         const int o = c + 32 * u + lane32;
                         jj[u] = o < n0 ? __ldg(bp + o) : EMPTY_KEY;
+                        aa[u] = a0;
+                        ss[u] = b0 + o;
                     }
-#pragma unroll
-                    for (int u = 0; u < U; u++) pr.put(jj[u], a0, b0 + c + 32 * u + lane32);
+                    pr.template put_batch<U>(jj, aa, ss);
                 }
             }
             const int slen = plen < 32 ? plen : 0;
@@ -184,8 +186,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                     aa[u] = KIND == 1 ? __shfl_sync(FULL, sa, own) : 0;
                     jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
                 }
-#pragma unroll
-                for (int u = 0; u < 2; u++) pr.put(jj[u], aa[u], ss[u]);
+                pr.template put_batch<2>(jj, aa, ss);
             }
             if (GW == 1) break;
         }

@@ -266,6 +266,12 @@ struct WarpProber {
         }
     }
 
+    template <int U>
+    __device__ __forceinline__ void put_batch(const int32_t* j, const long long* a, const long long* s) {
+#pragma unroll
+        for (int u = 0; u < U; u++) put(j[u], a[u], s[u]);
+    }
+
     __device__ __forceinline__ void drain() {
         if (qn) {
             __syncwarp();

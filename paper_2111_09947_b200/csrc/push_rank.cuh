@@ -91,45 +91,59 @@ struct MsaProber {
     uint32_t span;
     const void* b_val;
     unsigned evaluated;
-    __device__ __forceinline__ void put(int32_t j, long long a, long long s) {
-        const uint32_t off = (uint32_t)(j - lo);     // j = EMPTY_KEY -> off > span
-        uint32_t word = 0, pre = 0, hitbit;
-        const uint32_t w4 = (off >> 5) << 2;
-        asm volatile(
-            "{\n\t.reg .pred pin;\n\t"
-            "setp.le.u32 pin, %1, %2;\n\t"
-            "@pin ld.shared.u32 %0, [%3];\n\t}"
-            : "+r"(word)
-            : "r"(off), "r"(span), "r"(bits_s + w4));
-        const uint32_t b = off & 31u;
-        hitbit = (word >> b) & 1u;
-        asm volatile(
-            "{\n\t.reg .pred ph;\n\t"
-            "setp.ne.u32 ph, %1, 0;\n\t"
-            "@ph ld.shared.u32 %0, [%2];\n\t}"
-            : "+r"(pre)
-            : "r"(hitbit), "r"(pre_s + w4));
-        const uint32_t rank = pre + __popc(word & ((1u << b) - 1u));
-        evaluated += hitbit;
-        if (KIND == 0) {
-            if (NUMERIC)
-                asm volatile(
-                    "{\n\t.reg .pred ph;\n\t"
-                    "setp.ne.u32 ph, %0, 0;\n\t"
-                    "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"(hitbit),
-                    "r"(cnt_s + (rank << 2))
-                    : "memory");
-            else
-                asm volatile(
-                    "{\n\t.reg .pred ph;\n\t"
-                    "setp.ne.u32 ph, %0, 0;\n\t"
-                    "@ph st.shared.u32 [%1], 1;\n\t}" ::"r"(hitbit),
-                    "r"(cnt_s + (rank << 2))
-                    : "memory");
-        } else {
-            if (hitbit) {
+    // U products at once, stage by stage, so the shared loads of the U
+    // products are in flight together (ILP) instead of one dependency chain
+    // after another.
+    template <int U>
+    __device__ __forceinline__ void put_batch(const int32_t* j, const long long* a, const long long* s) {
+        uint32_t off[U], w4[U], word[U], pre[U], hit[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            off[u] = (uint32_t)(j[u] - lo);      // EMPTY_KEY -> off > span
+            w4[u] = (off[u] >> 5) << 2;
+            word[u] = 0u;
+            pre[u] = 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            asm volatile(
+                "{\n\t.reg .pred pin;\n\t"
+                "setp.le.u32 pin, %1, %2;\n\t"
+                "@pin ld.shared.u32 %0, [%3];\n\t}"
+                : "+r"(word[u])
+                : "r"(off[u]), "r"(span), "r"(bits_s + w4[u]));
+#pragma unroll
+        for (int u = 0; u < U; u++) hit[u] = (word[u] >> (off[u] & 31u)) & 1u;
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            asm volatile(
+                "{\n\t.reg .pred ph;\n\t"
+                "setp.ne.u32 ph, %1, 0;\n\t"
+                "@ph ld.shared.u32 %0, [%2];\n\t}"
+                : "+r"(pre[u])
+                : "r"(hit[u]), "r"(pre_s + w4[u]));
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t rank = pre[u] + __popc(word[u] & ((1u << (off[u] & 31u)) - 1u));
+            evaluated += hit[u];
+            if (KIND == 0) {
+                if (NUMERIC)
+                    asm volatile(
+                        "{\n\t.reg .pred ph;\n\t"
+                        "setp.ne.u32 ph, %0, 0;\n\t"
+                        "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"(hit[u]),
+                        "r"(cnt_s + (rank << 2))
+                        : "memory");
+                else
+                    asm volatile(
+                        "{\n\t.reg .pred ph;\n\t"
+                        "setp.ne.u32 ph, %0, 0;\n\t"
+                        "@ph st.shared.u32 [%1], 1;\n\t}" ::"r"(hit[u]),
+                        "r"(cnt_s + (rank << 2))
+                        : "memory");
+            } else if (hit[u]) {
                 if (NUMERIC) {
-                    const long long prod = a * ((const long long*)b_val)[s];
+                    const long long prod = a[u] * ((const long long*)b_val)[s[u]];
                     asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(val_s + (rank << 3)), "l"(prod) : "memory");
                 }
                 asm volatile("st.shared.u32 [%0], 1;" ::"r"(cnt_s + (rank << 2)) : "memory");
@@ -152,6 +166,11 @@ struct RankProber {
             evaluated++;
             rank_accumulate<KIND, NUMERIC>(sl, k, a, b_val, s);
         }
+    }
+    template <int U>
+    __device__ __forceinline__ void put_batch(const int32_t* j, const long long* a, const long long* s) {
+#pragma unroll
+        for (int u = 0; u < U; u++) put(j[u], a[u], s[u]);
     }
     __device__ __forceinline__ void drain() {}
 };
