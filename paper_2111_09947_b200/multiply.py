@@ -229,7 +229,7 @@ def _prepare(mask, a, b, plan: MultiplyPlan, device=None):
     b_csr = to_csr(b) if is_csc else b
     db = DeviceCsr.from_host(b_csr, dtype=dt, device=device, with_values=need_vals)
     dbt = None
-    if plan.algorithm in ("inner", "auto"):
+    if plan.algorithm == "inner" or (plan.algorithm == "auto" and is_csc):
         dbt = (DeviceCsr.from_host(b, dtype=dt, device=device, with_values=need_vals)
                if is_csc else db.transpose_storage())
     return dm, da, db, dbt, comp

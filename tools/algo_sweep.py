@@ -18,19 +18,20 @@ lib = _lib.load()
 h = _handle(0)
 lib.mm_profile_enable(h, 1)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-algos = os.environ.get("ALGOS", "hash,msa,mca,auto").split(",")
+algos = os.environ.get("ALGOS", "hash,msa,mca,auto,auto+pull").split(",")
 tunings = [[int(x) for x in t.split(":")] for t in os.environ.get("TUNINGS", "").split(",") if t]
 for tune in tunings or [None]:
     if tune:
         prm = (C.c_int64 * len(tune))(*tune)
         lib.mm_set_tuning(h, prm, len(tune))
     for algo in algos:
-        plan = MultiplyPlan(algorithm=algo, semiring=plus_pair_semiring(np.int64))
+        use_bt = algo in ("inner", "auto+pull")
+        plan = MultiplyPlan(algorithm=algo.replace("+pull", ""), semiring=plus_pair_semiring(np.int64))
         ms = (C.c_float * 6)()
         best_n, best_t = 1e9, 1e9
         for rep in range(4):
             flush.fill_(rep)
-            c, st = multiply_device(dl, dl, dl, plan, b_csc=bt if algo in ("inner", "auto") else None)
+            c, st = multiply_device(dl, dl, dl, plan, b_csc=bt if use_bt else None)
             lib.mm_profile_read(h, ms, 6, None)
             if rep:
                 best_n, best_t = min(best_n, ms[2]), min(best_t, ms[5])

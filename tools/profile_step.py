@@ -19,7 +19,7 @@ ap.add_argument("--reps", type=int, default=2)
 args = ap.parse_args()
 low = workloads.triangle_lower(args.scale)
 dl = DeviceCsr.from_host(low, with_values=False)
-bt = dl.transpose_storage() if args.algo in ("inner", "auto") else None
+bt = dl.transpose_storage() if args.algo == "inner" else None
 plan = MultiplyPlan(algorithm=args.algo, semiring=plus_pair_semiring(np.int64))
 for _ in range(args.reps):
     c, st = multiply_device(dl, dl, dl, plan, b_csc=bt)
