@@ -118,6 +118,15 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         }
     }
     if (fam == FAM_PULL) return BIN_PULL;
+    if (fam == FAM_HEAP) {
+        // plain: mask-rank slots in shared memory (tier 0) or global (tier 1);
+        // complement rows with <= 32 A entries: sorted single-batch merge (2)
+        if (!ap.comp) {
+            const int64_t bytes = (kind == 0 ? 4 : 12) * nm;
+            return BIN_HEAP0 + (bytes <= ap.rank_budget[0] ? 0 : 1);
+        }
+        if (na <= 32) return BIN_HEAP0 + 2;
+    }
     if (!ap.comp && (fam == FAM_MSA || fam == FAM_MCA)) {
         const int64_t bytes = fam == FAM_MSA ? msa_bytes(words, nm, kind) : mca_bytes(nm, kind);
         const int tier = bytes <= ap.rank_budget[tr] ? tr : 3;

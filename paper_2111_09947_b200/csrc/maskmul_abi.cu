@@ -21,6 +21,7 @@
 #include "pull_inner.cuh"
 #include "push_hash.cuh"
 #include "push_rank.cuh"
+#include "push_heap.cuh"
 #include "scan_compact.cuh"
 
 using namespace mm;
@@ -321,6 +322,40 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             CU(cudaGetLastError());
             continue;
         }
+        if (is_heap_bin(b)) {
+            const int sub = b - BIN_HEAP0;
+            const bool comp_rows = sub == 2;
+            const int kind = numeric ? h->kind : 0;
+            const int nm_max = std::max(h->sum.bin_nmmax[b], 1);
+            void (*kern)(Prob, Out, Work, int, int, unsigned char*) = nullptr;
+            if (comp_rows) {
+                if (!numeric) kern = k_push_heap<0, false, true>;
+                else if (kind == 0) kern = k_push_heap<0, true, true>;
+                else if (kind == 1) kern = k_push_heap<1, true, true>;
+                else kern = k_push_heap<2, true, true>;
+            } else {
+                if (!numeric) kern = k_push_heap<0, false, false>;
+                else if (kind == 0) kern = k_push_heap<0, true, false>;
+                else if (kind == 1) kern = k_push_heap<1, true, false>;
+                else kern = k_push_heap<2, true, false>;
+            }
+            const size_t wbytes = comp_rows ? 0 : (((size_t)(kind == 0 ? 4 : 12) * nm_max + 15) & ~(size_t)15);
+            const bool in_smem = sub == 0;
+            const size_t smem = in_smem ? 8 * wbytes : 0;
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            const int grid = std::max(1, std::min((cnt + 7) / 8, std::max(occ, 1) * h->num_sms));
+            unsigned char* gslab = nullptr;
+            if (!in_smem && !comp_rows) {
+                CU(cudaMallocAsync((void**)&gslab, (size_t)grid * 8 * wbytes, st));
+                h->allocs.push_back(gslab);
+            }
+            ++g_launches;
+            kern<<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max, h->plan.n_inspect, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
         return fail(MM_ERR_INTERNAL, "unhandled bin " + std::to_string(b));
     }
     return MM_OK;
@@ -369,6 +404,8 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
         case MM_ALGO_AUTO: ap.family = FAM_AUTO; break;
         case MM_ALGO_MSA: ap.family = FAM_MSA; break;
         case MM_ALGO_MCA: ap.family = FAM_MCA; break;
+        case MM_ALGO_HEAP:
+        case MM_ALGO_HEAPDOT: ap.family = FAM_HEAP; break;
         default: ap.family = FAM_HASH; break;   // hash; heap forms: see classify_row
     }
     ap.tier_flops0 = h->tier_flops0;
