@@ -258,3 +258,31 @@ def test_cfg2_triangle_count_bitwise():
         assert int(reduce_sum(c.values).item()) == g["sum_c"] == 423909251
         h = c.to_host()
         assert _digest(h) == g["digest_c"], algo
+
+
+def test_cfg2_two_phase_and_algorithms():
+    g = load_json("configs.json")["cfg2"]
+    w = workloads.cfg2()
+    dl = DeviceCsr.from_host(w.a, with_values=False)
+    for algo, ph in (("msa", "2p"), ("hash", "2p"), ("mca", "1p"), ("auto", "2p")):
+        c, st = multiply_device(dl, dl, dl, MultiplyPlan(algorithm=algo, phases=ph, semiring=w.semiring))
+        assert st.evaluated_multiplies == g["evaluated"], (algo, ph)
+        assert _digest(c.to_host()) == g["digest_c"], (algo, ph)
+
+
+@pytest.mark.slow
+def test_cfg5_ktruss_support_bitwise():
+    """R-MAT scale 22 k-truss support C = A (.) (A A): hub rows (163,558-entry
+    mask rows, 85M products) run on the global-memory tiers."""
+    g = load_json("configs.json").get("cfg5")
+    if g is None:
+        pytest.skip("cfg5 golden not generated")
+    w = workloads.cfg5()
+    assert digest_mat(w.a) == g["digest_a"]
+    da = DeviceCsr.from_host(w.a, with_values=False)
+    c, st = multiply_device(da, da, da, MultiplyPlan(algorithm="auto", semiring=w.semiring))
+    assert st.generated_flops == g["generated"]
+    assert st.evaluated_multiplies == g["evaluated"]
+    assert c.nnz == g["nnz_c"]
+    assert int(reduce_sum(c.values).item()) == g["sum_c"]
+    assert _digest(c.to_host()) == g["digest_c"]
