@@ -46,7 +46,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("MM_LIB_PATH") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"maskmul CUDA library missing at {path}: run __graft_entry__.build()")
     lib = C.CDLL(path)

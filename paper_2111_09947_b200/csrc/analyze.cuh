@@ -184,51 +184,107 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
     for (int b = threadIdx.x; b < NBINS; b += blockDim.x) { s_count[b] = 0; s_cap[b] = 0; s_bflops[b] = 0; s_words[b] = 0; s_nmx[b] = 0; }
     if (threadIdx.x == 0) { s_flops = 0; s_bound = 0; s_na = 0; s_nm = 0; }
     __syncthreads();
+    // A warp takes 32 consecutive rows, one per lane: short rows (<= 32 A
+    // entries / mask entries) are summed by their own lane with unrolled,
+    // independent loads; longer ones by the whole warp.  Classification runs
+    // lane-parallel; bin counters use warp-aggregated shared atomics.
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool want_pull = ap.family == FAM_AUTO && ap.has_bt && !ap.comp;
     unsigned long long my_flops = 0, my_bound = 0;
-    for (int64_t i = warp; i < p.nrows; i += nwarps) {
-        int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1];
+    for (int64_t r0 = warp * 32; r0 < p.nrows; r0 += nwarps * 32) {
+        const int64_t i = r0 + lane;
+        const bool live = i < p.nrows;
+        int64_t as = 0, ae = 0, ms = 0, me = 0;
+        if (live) {
+            as = p.a_ptr[i];
+            ae = p.a_ptr[i + 1];
+            ms = p.m_ptr[i];
+            me = p.m_ptr[i + 1];
+        }
         long long f = 0;
-        for (int64_t t = as + lane; t < ae; t += 32) {
-            int32_t k = p.a_idx[t];
-            f += p.b_ptr[k + 1] - p.b_ptr[k];
-        }
-        f = warp_sum_ll(f);
-        int64_t ms = p.m_ptr[i], me = p.m_ptr[i + 1];
-        int64_t nm = me - ms;
-        long long pull_cols = 0;
-        if (ap.family == FAM_AUTO && ap.has_bt && !ap.comp && f > 0 && nm > 0) {
-            for (int64_t t = ms + lane; t < me; t += 32) {
-                int32_t j = p.m_idx[t];
-                pull_cols += p.bt_ptr[j + 1] - p.bt_ptr[j];
+        if (ae - as <= 32) {
+            int64_t t = as;
+            for (; t + 4 <= ae; t += 4) {
+                const int32_t k0 = p.a_idx[t], k1 = p.a_idx[t + 1], k2 = p.a_idx[t + 2], k3 = p.a_idx[t + 3];
+                f += (p.b_ptr[k0 + 1] - p.b_ptr[k0]) + (p.b_ptr[k1 + 1] - p.b_ptr[k1]) +
+                     (p.b_ptr[k2 + 1] - p.b_ptr[k2]) + (p.b_ptr[k3 + 1] - p.b_ptr[k3]);
             }
-            pull_cols = warp_sum_ll(pull_cols);
+            for (; t < ae; t++) {
+                const int32_t k = p.a_idx[t];
+                f += p.b_ptr[k + 1] - p.b_ptr[k];
+            }
         }
-        if (lane == 0) {
-            int64_t na = ae - as;
+        unsigned longm = __ballot_sync(FULL, ae - as > 32);
+        while (longm) {
+            const int src = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int64_t s0 = shfl64(as, src), s1 = shfl64(ae, src);
+            long long g = 0;
+            for (int64_t t = s0 + lane; t < s1; t += 32) {
+                const int32_t k = p.a_idx[t];
+                g += p.b_ptr[k + 1] - p.b_ptr[k];
+            }
+            g = warp_sum_ll(g);
+            if (lane == src) f = g;
+        }
+        const int64_t nm = me - ms;
+        long long pull_cols = 0;
+        if (want_pull) {
+            if (f > 0 && nm > 0 && nm <= 32)
+                for (int64_t t = ms; t < me; t++) {
+                    const int32_t j = p.m_idx[t];
+                    pull_cols += p.bt_ptr[j + 1] - p.bt_ptr[j];
+                }
+            unsigned lm = __ballot_sync(FULL, f > 0 && nm > 32);
+            while (lm) {
+                const int src = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const int64_t s0 = shfl64(ms, src), s1 = shfl64(me, src);
+                long long g = 0;
+                for (int64_t t = s0 + lane; t < s1; t += 32) {
+                    const int32_t j = p.m_idx[t];
+                    g += p.bt_ptr[j + 1] - p.bt_ptr[j];
+                }
+                g = warp_sum_ll(g);
+                if (lane == src) pull_cols = g;
+            }
+        }
+        int b = -1;
+        if (live) {
+            const int64_t na = ae - as;
             row_flops[i] = f;
             if (bound) {
-                int64_t bd = f < p.ncols ? f : p.ncols;
+                const int64_t bd = f < p.ncols ? f : p.ncols;
                 bound[i] = bd;
                 my_bound += bd;
             }
             int cap_lg;
-            int64_t words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
-            int b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg);
-            atomicMax(&s_words[b], (int)(words < 0x7fffffff ? words : 0x7fffffff));
-            atomicMax(&s_nmx[b], (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
+            const int64_t words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
+            b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg);
             row_bin[i] = (uint8_t)b;
             row_cap_lg[i] = (int8_t)cap_lg;
-            atomicAdd(&s_count[b], 1);
             atomicAdd(&s_bflops[b], (unsigned long long)f);
-            atomicMax(&s_cap[b], cap_lg);
-            atomicMax(&s_na, (int)(na < 0x7fffffff ? na : 0x7fffffff));
-            atomicMax(&s_nm, (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
+            if (cap_lg) atomicMax(&s_cap[b], cap_lg);
+            if (b != BIN_EMPTY) {
+                atomicMax(&s_words[b], (int)(words < 0x7fffffff ? words : 0x7fffffff));
+                atomicMax(&s_nmx[b], (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
+            }
             my_flops += f;
         }
+        // warp-aggregated row counts and maxima
+        const unsigned peers = __match_any_sync(FULL, b);
+        if (live && lane == __ffs(peers) - 1) atomicAdd(&s_count[b], __popc(peers));
+        const int na_max = __reduce_max_sync(FULL, live ? (int)min(ae - as, (int64_t)0x7fffffff) : 0);
+        const int nm_max = __reduce_max_sync(FULL, live ? (int)min(nm, (int64_t)0x7fffffff) : 0);
+        if (lane == 0) {
+            atomicMax(&s_na, na_max);
+            atomicMax(&s_nm, nm_max);
+        }
     }
+    my_flops = (unsigned long long)warp_sum_ll((long long)my_flops);
+    my_bound = (unsigned long long)warp_sum_ll((long long)my_bound);
     if (lane == 0) {
         atomicAdd(&s_flops, my_flops);
         atomicAdd(&s_bound, my_bound);

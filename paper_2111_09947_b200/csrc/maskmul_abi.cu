@@ -443,7 +443,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     if (m > 0) CU(cudaMemsetAsync(h->row_nnz, 0, m * sizeof(int64_t), st));
 
     if (m > 0) {
-        int grid = (int)std::min<int64_t>((m + 7) / 8, (int64_t)h->num_sms * 16);
+        int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
         ++g_launches;
         k_analyze<<<grid, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin, h->row_cap_lg,
                                         h->d_summary);
@@ -718,7 +718,7 @@ int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops,
     CU(cudaMallocAsync((void**)&rc_lg, std::max<int64_t>(a->nrows, 1), st));
     CU(cudaMemsetAsync(s, 0, sizeof(Summary), st));
     if (a->nrows > 0) {
-        int grid = (int)std::min<int64_t>((a->nrows + 7) / 8, 148 * 16);
+        int grid = (int)std::min<int64_t>((a->nrows + 255) / 256, 148 * 8);
         ++g_launches;
         k_analyze<<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s);
     }

@@ -96,6 +96,12 @@ struct MsaProber {
     // after another.
     template <int U>
     __device__ __forceinline__ void put_batch(const int32_t* j, const long long* a, const long long* s) {
+#ifdef MM_EXPERIMENT_NOPROBE
+        // profiling-only build (tools/): enumerate and load products, skip the accumulator
+#pragma unroll
+        for (int u = 0; u < U; u++) evaluated += (j[u] != EMPTY_KEY);
+        return;
+#endif
         uint32_t off[U], w4[U], word[U], pre[U], hit[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
