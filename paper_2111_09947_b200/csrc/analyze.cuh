@@ -88,7 +88,7 @@ __device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
 
 // Shared-memory bytes per row of the rank-slot accumulators.
 __host__ __device__ constexpr int64_t msa_bytes(int64_t words, int64_t nm, int kind) {
-    return 8 * words + (kind == 0 ? 4 : 12) * nm;
+    return 6 * words + (kind == 0 ? 4 : 12) * nm;   // shared tiers: u16 rank prefix
 }
 __host__ __device__ constexpr int64_t mca_bytes(int64_t nm, int kind) {
     return (kind == 0 ? 8 : 16) * nm;

@@ -23,6 +23,8 @@
 #include "common.cuh"
 #include "product_loop.cuh"
 
+#include <type_traits>
+
 namespace mm {
 
 template <int KIND>
@@ -48,9 +50,10 @@ __device__ __forceinline__ void rank_accumulate(RankSlots<KIND>& sl, int r, long
 }
 
 // --- MSA bitmap probe ------------------------------------------------------
+template <class PreT>
 struct MsaBits {
     const uint32_t* bits;
-    const int32_t* pre;
+    const PreT* pre;
     int32_t lo;
     uint32_t span;   // hi - lo
     // slot of column j, or -1
@@ -61,7 +64,7 @@ struct MsaBits {
         const uint32_t word = bits[w];
         const uint32_t b = off & 31u;
         if (!((word >> b) & 1u)) return -1;
-        return pre[w] + __popc(word & ((1u << b) - 1u));
+        return (int)pre[w] + __popc(word & ((1u << b) - 1u));
     }
 };
 
@@ -102,7 +105,7 @@ struct MsaProber {
         for (int u = 0; u < U; u++) evaluated += (j[u] != EMPTY_KEY);
         return;
 #endif
-        uint32_t off[U], w4[U], word[U], pre[U], hit[U];
+        uint32_t off[U], w4[U], word[U], pre[U], hit[U];   // pre: u16 rank prefix per word
 #pragma unroll
         for (int u = 0; u < U; u++) {
             off[u] = (uint32_t)(j[u] - lo);      // EMPTY_KEY -> off > span
@@ -125,9 +128,9 @@ struct MsaProber {
             asm volatile(
                 "{\n\t.reg .pred ph;\n\t"
                 "setp.ne.u32 ph, %1, 0;\n\t"
-                "@ph ld.shared.u32 %0, [%2];\n\t}"
+                "@ph ld.shared.u16 %0, [%2];\n\t}"
                 : "+r"(pre[u])
-                : "r"(hit[u]), "r"(pre_s + w4[u]));
+                : "r"(hit[u]), "r"(pre_s + (w4[u] >> 1)));
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t rank = pre[u] + __popc(word[u] & ((1u << (off[u] & 31u)) - 1u));
@@ -198,14 +201,17 @@ struct RankLocatorF64 {
     __device__ __forceinline__ void mark(int k) { cnt[k] = 1; }
 };
 
-// Per-group region: [val: 8*NM if KIND != 0][cnt: 4*NM][MSA: bits 4*W, pre 4*W | MCA: mask 4*NM]
+// Per-group region: [val: 8*NM if KIND != 0][cnt: 4*NM]
+//   MSA: [bits 4*W][pre: 2*W (u16, shared tiers) or 4*W (global tier)]   MCA: [mask 4*NM]
 template <int KIND>
-__host__ __device__ constexpr size_t rank_region_bytes(bool msa, int64_t words, int64_t nm) {
-    return (size_t)(KIND == 0 ? 0 : 8) * nm + 4 * (size_t)nm + (msa ? 8 * (size_t)words : 4 * (size_t)nm);
+__host__ __device__ constexpr size_t rank_region_bytes(bool msa, bool smem, int64_t words, int64_t nm) {
+    return (size_t)(KIND == 0 ? 0 : 8) * nm + 4 * (size_t)nm +
+           (msa ? (smem ? 6 : 8) * (size_t)((words + 1) & ~1ll) : 4 * (size_t)nm);
 }
 
 template <int GW, int KIND, bool MSA, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned char* region, int nm_max,
+                                         int words_max,
                                          int64_t i, int gt, int bar_id, int* s_warp, BatchSmem bsm,
                                          unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
@@ -219,18 +225,16 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     unsigned char* aux = (unsigned char*)(sl.cnt + nm_max);
     const int32_t lo = p.m_idx[ms];
     const int32_t hi = p.m_idx[me - 1];
-    const int words = ((hi - lo) >> 5) + 1;
-    uint32_t* bits = (uint32_t*)aux;
-    int32_t* pre = (int32_t*)(aux + 4 * (size_t)(MSA ? words : 0));
+    using PreT = typename std::conditional<SMEM, uint16_t, int32_t>::type;
+    uint32_t* bits = (uint32_t*)aux;          // all-zero on entry (cleared by the previous row)
+    PreT* pre = (PreT*)(aux + 4 * (size_t)((words_max + 1) & ~1));
     int32_t* mrow = (int32_t*)aux;
 
-    // 1. clear slots (and the bitmap window), 2. mark the mask row
+    // 1. clear slots, 2. mark the mask row
     for (int r = gt; r < nm; r += GT) {
         sl.cnt[r] = 0;
         if (KIND == 1) sl.val[r] = 0ull;
     }
-    if (MSA)
-        for (int w = gt; w < words; w += GT) bits[w] = 0u;
     group_bar(bar_id, GT);
     for (int r = gt; r < nm; r += GT) {
         const int32_t j = p.m_idx[ms + r];
@@ -238,7 +242,7 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
             const uint32_t off = (uint32_t)(j - lo);
             const uint32_t w = off >> 5;
             atomicOr(bits + w, 1u << (off & 31u));
-            if (r == 0 || (((uint32_t)(p.m_idx[ms + r - 1] - lo)) >> 5) != w) pre[w] = r;
+            if (r == 0 || (((uint32_t)(p.m_idx[ms + r - 1] - lo)) >> 5) != w) pre[w] = (PreT)r;
         } else {
             mrow[r] = j;
         }
@@ -247,13 +251,13 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
 
     // 3. products
     if (MSA) {
-        MsaBits rb{bits, pre, lo, (uint32_t)(hi - lo)};
+        MsaBits<PreT> rb{bits, pre, lo, (uint32_t)(hi - lo)};
         if (KIND == 2) {
-            RankLocatorF64<MsaBits> loc{rb, sl.cnt, (double*)sl.val};
+            RankLocatorF64<MsaBits<PreT>> loc{rb, sl.cnt, (double*)sl.val};
             evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
         } else {
           if (!SMEM) {
-            RankProber<KIND, NUMERIC, MsaBits> pr{rb, sl, p.b_val, 0u};
+            RankProber<KIND, NUMERIC, MsaBits<PreT>> pr{rb, sl, p.b_val, 0u};
             flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
             evaluated += pr.evaluated;
           } else {
@@ -285,27 +289,48 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     }
     group_bar(bar_id, GT);
 
-    // 4. gather in mask order
+    // 4. gather in mask order: warp w owns ranks [w nm/GW, (w+1) nm/GW)
     const int64_t w0 = NUMERIC ? o.off[i] : 0;
-    int running = 0;
-    for (int base = 0; base < nm; base += GT) {
-        const int r = base + gt;
-        const bool set = r < nm && sl.cnt[r] > 0;
-        int tot;
-        const int pos = group_prefix<GW>(set, &tot, s_warp, bar_id, gt);
-        if (NUMERIC && set) {
-            const int64_t d = w0 + running + pos;
-            o.idx[d] = p.m_idx[ms + r];
-            if (KIND == 0) {
-                if (o.out_f64) ((double*)o.val)[d] = (double)sl.cnt[r];
-                else ((long long*)o.val)[d] = sl.cnt[r];
-            } else {
-                ((unsigned long long*)o.val)[d] = sl.val[r];
-            }
+    const int wg = gt >> 5;
+    const int r_lo = (int)(((long long)nm * wg) / GW), r_hi = (int)(((long long)nm * (wg + 1)) / GW);
+    int mine = 0;
+    for (int r = r_lo + lane; r < r_hi; r += 32) mine += sl.cnt[r] > 0;
+    mine = (int)warp_sum_ll(mine);
+    int before = 0, total = mine;
+    if (GW > 1) {
+        if (lane == 0) s_warp[wg] = mine;
+        group_bar(bar_id, GT);
+        total = 0;
+#pragma unroll
+        for (int q = 0; q < GW; q++) {
+            const int c = s_warp[q];
+            if (q < wg) before += c;
+            total += c;
         }
-        running += tot;
     }
-    if (gt == 0) o.row_nnz[i] = running;
+    if (NUMERIC) {
+        int run = before;
+        for (int rb0 = r_lo; rb0 < r_hi; rb0 += 32) {
+            const int r = rb0 + lane;
+            const bool set = r < r_hi && sl.cnt[r] > 0;
+            const unsigned bal = __ballot_sync(FULL, set);
+            if (set) {
+                const int64_t d = w0 + run + __popc(bal & lanemask_lt());
+                o.idx[d] = p.m_idx[ms + r];
+                if (KIND == 0) {
+                    if (o.out_f64) ((double*)o.val)[d] = (double)sl.cnt[r];
+                    else ((long long*)o.val)[d] = sl.cnt[r];
+                } else {
+                    ((unsigned long long*)o.val)[d] = sl.val[r];
+                }
+            }
+            run += __popc(bal);
+        }
+    }
+    if (gt == 0) o.row_nnz[i] = total;
+    // 5. leave the bitmap all-zero for the next row (only the touched words)
+    if (MSA)
+        for (int r = gt; r < nm; r += GT) bits[((uint32_t)(p.m_idx[ms + r] - lo)) >> 5] = 0u;
     group_bar(bar_id, GT);
 }
 
@@ -322,7 +347,7 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     const int g = threadIdx.x / GT;
     const int gt = threadIdx.x % GT;
     const int bar_id = 1 + g;
-    const size_t rbytes = (rank_region_bytes<KIND>(MSA, words_max, nm_max) + 15) & ~(size_t)15;
+    const size_t rbytes = (rank_region_bytes<KIND>(MSA, SMEM, words_max, nm_max) + 15) & ~(size_t)15;
     unsigned char* region = SMEM ? smem + (size_t)g * rbytes : gslab + ((size_t)blockIdx.x * groups + g) * rbytes;
     unsigned char* bbase = smem + (SMEM ? (size_t)groups * rbytes : 0) + (size_t)g * batch_bytes<GW, KIND>();
     BatchSmem bsm;
@@ -330,14 +355,18 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     bsm.av = bsm.base + GT;
     bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
     unsigned long long evaluated = 0;
+    if (MSA) {
+        uint32_t* bits = (uint32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
+        for (int w = gt; w < words_max; w += GT) bits[w] = 0u;
+    }
     for (;;) {
         if (gt == 0) s_row[g] = atomicAdd(wk.cursor, 1);
         group_bar(bar_id, GT);
         const int r = s_row[g];
         group_bar(bar_id, GT);
         if (r >= wk.count) break;
-        rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, wk.rows[r], gt, bar_id, s_warp + g * GW, bsm,
-                                         evaluated);
+        rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, words_max, wk.rows[r], gt, bar_id,
+                                               s_warp + g * GW, bsm, evaluated);
     }
     if (NUMERIC) {
         const long long e = warp_sum_ll((long long)evaluated);
