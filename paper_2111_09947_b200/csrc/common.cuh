@@ -25,8 +25,6 @@ struct Prob {
     const int64_t* row_flops;
     int64_t nrows;
     int64_t ncols;
-    int64_t b_nnz;       // entries in b_idx (guards the 16-byte vector loads)
-    int b_vec;           // b_idx is 16-byte aligned: vector loads allowed
 };
 
 // Where a kernel writes its rows.  off[i] = slot offset of row i (1P bound

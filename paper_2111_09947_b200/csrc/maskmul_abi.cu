@@ -398,8 +398,6 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     p.bt_val = use_bt ? bt->values : nullptr;
     p.nrows = h->nrows;
     p.ncols = h->ncols;
-    p.b_nnz = b->nnz;
-    p.b_vec = ((uintptr_t)b->idx & 15) == 0;
     AnalyzeParams& ap = h->ap;
     switch (plan->algorithm) {
         case MM_ALGO_INNER: ap.family = FAM_PULL; break;

@@ -94,6 +94,8 @@ template <int GW, int KIND, class PR>
 __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as, int64_t ae, int gt,
                                               int bar_id, int* s_warp, BatchSmem bsm) {
     constexpr int GT = GW * 32;
+    constexpr int U = 4;
+    constexpr int CH = 32 * U;
     constexpr int NB = GT;
     const int lane32 = gt & 31;
     const int wg = gt >> 5;
@@ -155,52 +157,18 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 const long long b0 = shfl64(sb, src);
                 const int n0 = __shfl_sync(FULL, plen, src);
                 const long long a0 = KIND == 1 ? __shfl_sync(FULL, sa, src) : 0;
-                if (!p.b_vec) {
-                    // unaligned B (a view): scalar loads, 4 in flight per lane
-                    const int32_t* bp = p.b_idx + b0;
-                    for (int c = 0; c < n0; c += 128) {
-                        int32_t jj[4];
-                        long long aa[4], ss[4];
+                const int32_t* bp = p.b_idx + b0;
+                for (int c = 0; c < n0; c += CH) {
+                    int32_t jj[U];
+                    long long aa[U], ss[U];
 #pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const int o = c + 32 * u + lane32;
-                            jj[u] = o < n0 ? __ldg(bp + o) : EMPTY_KEY;
-                            aa[u] = a0;
-                            ss[u] = b0 + o;
-                        }
-                        pr.template put_batch<4>(jj, aa, ss);
+                    for (int u = 0; u < U; u++) {
+                        const int o = c + 32 * u + lane32;
+                        jj[u] = o < n0 ? __ldg(bp + o) : EMPTY_KEY;
+                        aa[u] = a0;
+                        ss[u] = b0 + o;
                     }
-                    continue;
-                }
-                // 16-byte vector loads: lanes take 4-entry units of b_idx
-                // (aligned down; entries outside [b0, b0+n0) are masked), so
-                // one load instruction feeds 4 products per lane
-                const long long b_end = b0 + n0;
-                const long long u_hi = (b_end + 3) >> 2;
-                const int4* bp4 = reinterpret_cast<const int4*>(p.b_idx);
-                for (long long uc = b0 >> 2; uc < u_hi; uc += 32) {
-                    const long long un = uc + lane32;
-                    const long long e0 = un << 2;
-                    int4 q = make_int4(EMPTY_KEY, EMPTY_KEY, EMPTY_KEY, EMPTY_KEY);
-                    if (un < u_hi) {
-                        if (e0 + 3 < p.b_nnz) {
-                            q = __ldg(bp4 + un);
-                        } else {
-                            q.x = e0 < p.b_nnz ? __ldg(p.b_idx + e0) : EMPTY_KEY;
-                            q.y = e0 + 1 < p.b_nnz ? __ldg(p.b_idx + e0 + 1) : EMPTY_KEY;
-                            q.z = e0 + 2 < p.b_nnz ? __ldg(p.b_idx + e0 + 2) : EMPTY_KEY;
-                        }
-                    }
-                    int32_t jj[4];
-                    long long aa[4], ss[4];
-                    jj[0] = q.x; jj[1] = q.y; jj[2] = q.z; jj[3] = q.w;
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        ss[e] = e0 + e;
-                        aa[e] = a0;
-                        if (ss[e] < b0 || ss[e] >= b_end) jj[e] = EMPTY_KEY;
-                    }
-                    pr.template put_batch<4>(jj, aa, ss);
+                    pr.template put_batch<U>(jj, aa, ss);
                 }
             }
             const int slen = plen < 32 ? plen : 0;
