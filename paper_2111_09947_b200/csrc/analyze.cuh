@@ -74,6 +74,7 @@ struct AnalyzeParams {
     int capc_lg;             // table-size class boundary (log2 slots)
     int load_shift;          // preferred table size = keys << load_shift
     int rank_budget[3];      // MSA / MCA shared bytes per group allowed in tiers 0..2
+    int auto_mca_nm;         // AUTO: 1-warp rows whose MSA window is too wide use MCA if nm <= this
     int family;      // Family
     int comp;        // complemented mask
     int ordered;     // fp64 plus-times: single-warp ordered accumulation
@@ -115,6 +116,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             if (ap.has_bt && pull < push) fam = FAM_PULL;
             // push: the bitmap accumulator when the mask window is compact
             else if (msa_bytes(words, nm, kind) <= ap.rank_budget[tr]) fam = FAM_MSA;
+            else if (tr == 0 && nm <= ap.auto_mca_nm) fam = FAM_MCA;
         }
     }
     if (fam == FAM_PULL) return BIN_PULL;

@@ -83,6 +83,7 @@ struct mm_handle {
     long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;
     int capc_lg = CAPC_LG, load_shift = 2;
     int rank_budget[3] = {6144, 24576, 49152};
+    int auto_mca_nm = 0;
     // ---- profiling ----
     bool prof = false;
     cudaEvent_t ev[6] = {};
@@ -413,6 +414,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     ap.capc_lg = h->capc_lg;
     ap.load_shift = h->load_shift;
     for (int t = 0; t < 3; t++) ap.rank_budget[t] = h->rank_budget[t];
+    ap.auto_mca_nm = h->auto_mca_nm;
     ap.comp = comp;
     ap.ordered = h->kind == 2;
     ap.pair = pair;
@@ -669,6 +671,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 3 && params[3] > 0 && params[3] <= 4) h->load_shift = (int)params[3];
     for (int t = 0; t < 3; t++)
         if (n > 4 + t && params[4 + t] > 0) h->rank_budget[t] = (int)params[4 + t];
+    if (n > 7 && params[7] >= 0) h->auto_mca_nm = (int)params[7];
     return MM_OK;
 }
 
