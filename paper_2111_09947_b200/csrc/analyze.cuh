@@ -165,7 +165,10 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         for (int t = 0; t < 3; t++) {
             if (need <= tier_cap_lg(ap.pair, t)) { tc = t; break; }
         }
-        tier = tc > tf ? tc : tf;
+        // a binary search per product is a chain of dependent loads: spread
+        // the row's products over more lanes much earlier than for probing
+        const int tfm = mode == MODE_CSRCH ? (flops <= 64 ? 0 : (flops <= 1024 ? 1 : 2)) : tf;
+        tier = tc > tfm ? tc : tfm;
     }
     int lim = tier_cap_lg(ap.pair, tier);
     const int used = want < lim ? want : lim;
