@@ -29,7 +29,8 @@ enum Bin : int {
     BIN_MSA0 = 23,    // + tier (0..3)
     BIN_MCA0 = 27,    // + tier
     BIN_HEAP0 = 31,   // + tier
-    NBINS = 35
+    BIN_SINGLE = 35,  // one A entry: filtered, scaled copy of B_k (auto)
+    NBINS = 36
 };
 __host__ __device__ constexpr bool is_msa_bin(int b) { return b >= BIN_MSA0 && b < BIN_MSA0 + 4; }
 __host__ __device__ constexpr bool is_mca_bin(int b) { return b >= BIN_MCA0 && b < BIN_MCA0 + 4; }
@@ -106,6 +107,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     const int tf = flops <= ap.tier_flops0 ? 0 : (flops <= ap.tier_flops1 ? 1 : 2);
     const int tr = ap.ordered ? 0 : tf;        // ordered float64 runs one warp per row
     int fam = ap.family;
+    if (fam == FAM_AUTO && na == 1 && 4 * (nm > 0 ? words : 1) <= ap.rank_budget[1]) return BIN_SINGLE;
     if (fam == FAM_AUTO) {
         fam = FAM_HASH;
         if (!ap.comp) {

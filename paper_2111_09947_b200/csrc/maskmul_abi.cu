@@ -22,6 +22,7 @@
 #include "push_hash.cuh"
 #include "push_rank.cuh"
 #include "push_heap.cuh"
+#include "push_single.cuh"
 #include "scan_compact.cuh"
 
 using namespace mm;
@@ -354,6 +355,25 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             }
             ++g_launches;
             kern<<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max, h->plan.n_inspect, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
+        if (b == BIN_SINGLE) {
+            const int kind = numeric ? h->kind : 0;
+            const bool comp = h->plan.complemented != 0;
+            void (*kern)(Prob, Out, Work, int) = nullptr;
+            if (!numeric) kern = comp ? k_push_single<0, false, true> : k_push_single<0, false, false>;
+            else if (kind == 0) kern = comp ? k_push_single<0, true, true> : k_push_single<0, true, false>;
+            else if (kind == 1) kern = comp ? k_push_single<1, true, true> : k_push_single<1, true, false>;
+            else kern = comp ? k_push_single<2, true, true> : k_push_single<2, true, false>;
+            const int words_max = std::max(h->sum.bin_words[b], 1);
+            const size_t smem = 2 * 4 * (size_t)words_max;
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            const int grid = std::max(1, std::min((cnt + 1) / 2, std::max(occ, 1) * h->num_sms));
+            ++g_launches;
+            kern<<<grid, 256, smem, st>>>(h->prob, out, wk, words_max);
             CU(cudaGetLastError());
             continue;
         }
