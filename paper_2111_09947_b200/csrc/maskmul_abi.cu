@@ -367,7 +367,9 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             else if (kind == 1) kern = comp ? k_push_single<1, true, true> : k_push_single<1, true, false>;
             else kern = comp ? k_push_single<2, true, true> : k_push_single<2, true, false>;
             const int words_max = std::max(h->sum.bin_words[b], 1);
+            // two 4-warp groups per block while the bitmaps fit, else one group
             const size_t smem = 2 * 4 * (size_t)words_max;
+            if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "single-entry bitmap exceeds shared memory");
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
             CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
