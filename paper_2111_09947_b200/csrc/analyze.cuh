@@ -108,7 +108,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     const int tr = ap.ordered ? 0 : tf;        // ordered float64 runs one warp per row
     int fam = ap.family;
     // one A entry, many products, a wide mask window: the bitmap filter (cfg4 shape)
-    if (fam == FAM_AUTO && na == 1 && flops >= 128 && words >= 256 && 4 * words <= 98304) return BIN_SINGLE;
+    if (fam == FAM_AUTO && na == 1 && words >= 256 && 4 * words <= 98304) return BIN_SINGLE;
     if (fam == FAM_AUTO) {
         fam = FAM_HASH;
         if (!ap.comp) {
