@@ -167,6 +167,12 @@ int mm_compact_rows(int64_t nrows, const int64_t* bounds_off, const int64_t* row
                     const int32_t* tmp_idx, const void* tmp_val, const int64_t* out_ptr,
                     int32_t* out_idx, void* out_val, int dtype, void* stream);
 
+/* k-truss prune step (graphs.py:111-117): the pattern of C's entries with
+ * int64 value >= thr, as CSR (out_row_ptr[nrows+1], out_idx[capacity nnz(C)]);
+ * *out_nnz (host) receives the kept count.  Synchronous on `stream`. */
+int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32_t* out_idx,
+                  int64_t* out_nnz, void* stream);
+
 /* sum of values[0..n) into *out (device, int64 or float64) — the triangle
  * count reduction of triangle_count (graphs.py:96). */
 int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* stream);

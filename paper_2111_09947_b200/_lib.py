@@ -19,7 +19,7 @@ MM_DTYPE_INT64, MM_DTYPE_FLOAT64 = 0, 1
 EXPORTS = ("mm_abi_version", "mm_last_error", "mm_create", "mm_destroy", "mm_multiply_begin",
            "mm_multiply_end", "mm_symbolic", "mm_row_flops", "mm_exclusive_scan",
            "mm_compact_rows", "mm_reduce_sum", "mm_profile_enable", "mm_profile_read",
-           "mm_profile_bins", "mm_set_tuning")
+           "mm_profile_bins", "mm_set_tuning", "mm_filter_min")
 
 
 class MatrixT(C.Structure):
@@ -67,6 +67,7 @@ def load(path: str | None = None):
     lib.mm_profile_read.argtypes = [P, P, C.c_int, C.POINTER(C.c_int64)]
     lib.mm_profile_bins.argtypes = [P, P, P, C.c_int]
     lib.mm_set_tuning.argtypes = [P, P, C.c_int]
+    lib.mm_filter_min.argtypes = [C.POINTER(MatrixT), C.c_int64, P, P, C.POINTER(C.c_int64), P]
     for name in EXPORTS:
         getattr(lib, name)
         if name not in ("mm_last_error",):

@@ -785,6 +785,38 @@ int mm_compact_rows(int64_t nrows, const int64_t* bounds_off, const int64_t* row
     return MM_OK;
 }
 
+int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32_t* out_idx,
+                  int64_t* out_nnz, void* stream) {
+    if (!c || !out_row_ptr || !out_nnz) return fail(MM_ERR_INPUT, "null argument");
+    if (c->nnz > 0 && (!c->values || !c->idx || !out_idx)) return fail(MM_ERR_INPUT, "values and output indices required");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t m = c->nrows;
+    int64_t* counts = nullptr;
+    long long* hnz = nullptr;
+    CU(cudaMallocAsync((void**)&counts, std::max<int64_t>(m, 1) * sizeof(int64_t), st));
+    CU(cudaMallocHost((void**)&hnz, sizeof(long long)));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 7) / 8, 148 * 16));
+    if (m > 0) {
+        ++g_launches;
+        k_filter_min<false><<<grid, 256, 0, st>>>(m, c->ptr, c->idx, (const long long*)c->values, thr, counts,
+                                                  nullptr, nullptr);
+    }
+    int rc = exclusive_scan(counts, m, out_row_ptr, st);
+    if (rc) { cudaFreeAsync(counts, st); cudaFreeHost(hnz); return rc; }
+    if (m > 0) {
+        ++g_launches;
+        k_filter_min<true><<<grid, 256, 0, st>>>(m, c->ptr, c->idx, (const long long*)c->values, thr, nullptr,
+                                                 out_row_ptr, out_idx);
+    }
+    CU(cudaMemcpyAsync(hnz, out_row_ptr + m, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    *out_nnz = *hnz;
+    cudaFreeAsync(counts, st);
+    cudaFreeHost(hnz);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
 int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* stream) {
     if (!out) return fail(MM_ERR_INPUT, "null argument");
     cudaStream_t st = (cudaStream_t)stream;

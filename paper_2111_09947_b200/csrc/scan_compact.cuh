@@ -153,3 +153,31 @@ __global__ void __launch_bounds__(256) k_reduce_final(const T* partials, int npa
     if (threadIdx.x == 0) *out = s[0];
 }
 }  // namespace mm
+
+namespace mm {
+
+// k-truss prune step (graphs.py:111-117): keep the entries of C whose value
+// is >= thr.  Pass 1 counts survivors per row (warp per row), pass 2 copies
+// them in order into the scanned offsets; the kept pattern stays canonical.
+template <bool WRITE>
+__global__ void __launch_bounds__(256) k_filter_min(int64_t nrows, const int64_t* ptr, const int32_t* idx,
+                                                    const long long* val, long long thr, int64_t* counts,
+                                                    const int64_t* out_ptr, int32_t* out_idx) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < nrows; i += nwarps) {
+        const int64_t s0 = ptr[i], s1 = ptr[i + 1];
+        int64_t run = WRITE ? out_ptr[i] : 0;
+        for (int64_t b = s0; b < s1; b += 32) {
+            const int64_t s = b + lane;
+            const bool keep = s < s1 && val[s] >= thr;
+            const unsigned bal = __ballot_sync(FULL, keep);
+            if (WRITE && keep) out_idx[run + __popc(bal & lanemask_lt())] = idx[s];
+            run += __popc(bal);
+        }
+        if (!WRITE && lane == 0) counts[i] = run;
+    }
+}
+
+}  // namespace mm

@@ -48,34 +48,53 @@ def triangle_count(g: CsrMatrix, plan: MultiplyPlan, device=None) -> KernelResul
     kplan = replace(plan, semiring=plus_pair_semiring(np.int64), complemented=False)
     dl = DeviceCsr.from_host(low, device=device, with_values=False)
     c, st = multiply_device(dl, dl, dl, kplan,
-                            b_csc=dl.transpose_storage() if kplan.algorithm in ("inner", "auto") else None)
+                            b_csc=dl.transpose_storage() if kplan.algorithm == "inner" else None)
     total = int(reduce_sum(c.values).item()) if c.nnz else 0
     return KernelResult(total, st.total_seconds, st.generated_flops, st.evaluated_multiplies, 1,
                         [(st.total_seconds, st.generated_flops)])
 
 
 def k_truss(g: CsrMatrix, k: int, plan: MultiplyPlan, device=None) -> KernelResult:
+    """Edges with support >= k-2, pruned to a fixed point (graphs.py:99-118).
+
+    The whole loop stays on the device: support = G (.) (G G) under
+    plus-pair, then mm_filter_min keeps the entries with support >= k-2 as
+    the next (canonical) graph; one nnz readback per iteration decides the
+    fixed point.  Only the final graph comes back to the host."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from .multiply import _raise
+
     if k < 3:
         raise ValueError("k-truss needs k >= 3")
     _check_simple_symmetric(g, "k-truss")
     kplan = replace(plan, semiring=plus_pair_semiring(np.int64), complemented=False)
     res = KernelResult(None)
-    cur = g
+    cur = DeviceCsr.from_host(g, device=device, with_values=False)
+    lib = _lib.load()
     while cur.nnz:
-        dc = DeviceCsr.from_host(cur, device=device, with_values=False)
-        sup, st = multiply_device(dc, dc, dc, kplan,
-                                  b_csc=dc.transpose_storage() if kplan.algorithm in ("inner", "auto") else None)
+        sup, st = multiply_device(cur, cur, cur, kplan,
+                                  b_csc=cur.transpose_storage() if kplan.algorithm == "inner" else None)
         res.multiply_seconds += st.total_seconds
         res.flops += st.generated_flops
         res.evaluated += st.evaluated_multiplies
         res.multiplies += 1
         res.per_multiply.append((st.total_seconds, st.generated_flops))
-        support = sup.to_host()
-        rows, cols, vals = support.triples()
-        keep = vals >= k - 2
-        if int(keep.sum()) == cur.nnz:
+        dev = sup.idx.device
+        ptr = torch.empty(cur.nrows + 1, dtype=torch.int64, device=dev)
+        idx = torch.empty(max(sup.nnz, 1), dtype=torch.int32, device=dev)
+        nnz = C.c_int64(0)
+        rc = lib.mm_filter_min(C.byref(sup.mm()), k - 2, ptr.data_ptr(), idx.data_ptr(), C.byref(nnz),
+                               C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+        if rc:
+            _raise(rc)
+        if int(nnz.value) == cur.nnz:
             break
-        cur = from_arrays(cur.nrows, cur.ncols, rows[keep], cols[keep],
-                          np.ones(int(keep.sum()), dtype=np.int64))
-    res.value = cur
+        cur = DeviceCsr(cur.nrows, cur.ncols, ptr, idx[: int(nnz.value)].contiguous(), None)
+    host = cur.to_host()
+    host.values = np.ones(host.nnz, dtype=np.int64)
+    res.value = host
     return res

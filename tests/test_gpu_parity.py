@@ -286,3 +286,35 @@ def test_cfg5_ktruss_support_bitwise():
     assert c.nnz == g["nnz_c"]
     assert int(reduce_sum(c.values).item()) == g["sum_c"]
     assert _digest(c.to_host()) == g["digest_c"]
+
+
+def test_triangle_count_and_k_truss_graph_kernels():
+    from paper_2111_09947_b200.graphs import k_truss, triangle_count
+    from paper_2111_09947_b200.sparse import simple_undirected_graph
+    from paper_2111_09947_b200.workloads import GeneratorSpec, generate
+    k = load_json("kats.json")
+
+    def complete(n):
+        return from_triples(n, n, [(i, j, 1) for i in range(n) for j in range(n) if i != j])
+    plan = MultiplyPlan(algorithm="auto")
+    for n, want in k["tc_complete"].items():
+        assert triangle_count(complete(int(n)), plan).value == want
+    g = simple_undirected_graph(generate(GeneratorSpec("erdos-renyi", 10, 8, seed=42)))
+    assert triangle_count(g, plan).value == k["tc_er10_d8_seed42"]
+    assert k_truss(complete(5), 5, plan).value.nnz == 20      # test_graphs.py:72-74
+    assert k_truss(complete(4), 5, plan).value.nnz == 0
+    # R-MAT scale-8 graphs against a host fixed point built on the oracle
+    for seed in range(8):
+        g = simple_undirected_graph(generate(GeneratorSpec("rmat", 8, 4, seed=seed)))
+        cur = g
+        while cur.nnz:
+            r = oracle.masked_multiply(cur.pattern(), cur, cur, semiring_id=1)
+            keep = r.values >= 3
+            rows = np.repeat(np.arange(cur.nrows), np.diff(r.row_ptr))
+            if int(keep.sum()) == cur.nnz:
+                break
+            from paper_2111_09947_b200.sparse import from_arrays
+            cur = from_arrays(cur.nrows, cur.ncols, rows[keep], r.col_idx[keep],
+                              np.ones(int(keep.sum()), dtype=np.int64))
+        got = k_truss(g, 5, MultiplyPlan(algorithm="hash")).value
+        assert np.array_equal(got.row_ptr, cur.row_ptr) and np.array_equal(got.col_idx, cur.col_idx[: cur.nnz])
