@@ -94,7 +94,10 @@ template <int GW, int KIND, class PR>
 __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as, int64_t ae, int gt,
                                               int bar_id, int* s_warp, BatchSmem bsm) {
     constexpr int GT = GW * 32;
-    constexpr int U = 4;
+#ifndef MM_PRODUCT_UNROLL
+#define MM_PRODUCT_UNROLL 4
+#endif
+    constexpr int U = MM_PRODUCT_UNROLL;   // independent B loads in flight per lane
     constexpr int CH = 32 * U;
     constexpr int NB = GT;
     const int lane32 = gt & 31;
