@@ -85,6 +85,10 @@ struct mm_handle {
     int capc_lg = CAPC_LG, load_shift = 2;
     int rank_budget[3] = {6144, 24576, 49152};
     int auto_mca_nm = 0;
+    // ---- concurrent bin launches ----
+    static constexpr int NAUX = 3;
+    cudaStream_t aux[NAUX] = {};
+    cudaEvent_t fork_ev = nullptr, join_ev[NAUX] = {};
     // ---- profiling ----
     bool prof = false;
     cudaEvent_t ev[6] = {};
@@ -236,12 +240,38 @@ RankKernel pick_rank(int kind, int tier, bool numeric, int* gw) {
 }
 
 // Launch every non-empty bin.  numeric=false: symbolic counts into out.row_nnz.
+int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order, int norder);
+
+// Launch every non-empty bin.  Bins run concurrently on NAUX auxiliary
+// streams forked from / joined to the caller's stream, heaviest first, so the
+// tail of one bin's kernel overlaps the next bin's blocks.
 int launch_bins(mm_handle* h, bool numeric, const Out& out) {
-    cudaStream_t st = h->stream;
+    int order[NBINS], n = 0;
+    for (int b = 1; b < NBINS; b++)
+        if (h->sum.bin_count[b]) order[n++] = b;
+    std::sort(order, order + n, [&](int x, int y) { return h->sum.bin_flops[x] > h->sum.bin_flops[y]; });
+    return launch_bins_on(h, numeric, out, order, n);
+}
+
+int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order, int norder) {
+    cudaStream_t main_st = h->stream;
+    const bool concurrent = norder > 1;
+    if (concurrent) {
+        if (!h->fork_ev) {
+            CU(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
+            for (int q = 0; q < mm_handle::NAUX; q++) {
+                CU(cudaStreamCreateWithFlags(&h->aux[q], cudaStreamNonBlocking));
+                CU(cudaEventCreateWithFlags(&h->join_ev[q], cudaEventDisableTiming));
+            }
+        }
+        CU(cudaEventRecord(h->fork_ev, main_st));
+        for (int q = 0; q < mm_handle::NAUX && q < norder; q++) CU(cudaStreamWaitEvent(h->aux[q], h->fork_ev, 0));
+    }
     int32_t* cursors = h->cursors + (numeric ? NBINS : 0);
-    for (int b = 1; b < NBINS; b++) {
-        int cnt = h->sum.bin_count[b];
-        if (!cnt) continue;
+    for (int oi = 0; oi < norder; oi++) {
+        const int b = order[oi];
+        const int cnt = h->sum.bin_count[b];
+        cudaStream_t st = concurrent ? h->aux[oi % mm_handle::NAUX] : main_st;
         Work wk{h->rows_list + h->bin_off[b], cnt, cursors + b};
         if (b == BIN_PULL) {
             int kind = numeric ? h->kind : 0;
@@ -380,6 +410,12 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
             continue;
         }
         return fail(MM_ERR_INTERNAL, "unhandled bin " + std::to_string(b));
+    }
+    if (concurrent) {
+        for (int q = 0; q < mm_handle::NAUX && q < norder; q++) {
+            CU(cudaEventRecord(h->join_ev[q], h->aux[q]));
+            CU(cudaStreamWaitEvent(main_st, h->join_ev[q], 0));
+        }
     }
     return MM_OK;
 }
@@ -644,6 +680,13 @@ int mm_destroy(mm_handle_t* h) {
     cudaFreeHost(h->h_summary);
     cudaFreeHost(h->h_scalar);
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    if (h->fork_ev) {
+        cudaEventDestroy(h->fork_ev);
+        for (int q = 0; q < mm_handle::NAUX; q++) {
+            cudaEventDestroy(h->join_ev[q]);
+            cudaStreamDestroy(h->aux[q]);
+        }
+    }
     delete h;
     return MM_OK;
 }
