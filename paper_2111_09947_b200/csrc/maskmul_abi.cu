@@ -225,7 +225,10 @@ RankKernel pick_rank_unordered(int tier, int* gw) {
     switch (tier) {
         case 0: *gw = 1; return k_push_rank<1, true, KIND, MSA, NUM>;
         case 1: *gw = 4; return k_push_rank<4, true, KIND, MSA, NUM>;
-        case 2: *gw = 16; return k_push_rank<16, true, KIND, MSA, NUM>;
+#ifndef MM_RANK_T2_GW
+#define MM_RANK_T2_GW 16
+#endif
+        case 2: *gw = MM_RANK_T2_GW; return k_push_rank<MM_RANK_T2_GW, true, KIND, MSA, NUM>;
         default: *gw = 32; return k_push_rank<32, false, KIND, MSA, NUM>;
     }
 }
