@@ -50,7 +50,7 @@ __host__ __device__ constexpr int hash_bin_tier(int b) {
 __host__ __device__ constexpr int tier_gw(int t) { return t == 0 ? 1 : (t == 1 ? 4 : (t == 2 ? 16 : 32)); }
 __host__ __device__ constexpr int tier_cap_lg_pair(int t) { return t == 0 ? 10 : (t == 1 ? 13 : (t == 2 ? 14 : 30)); }
 __host__ __device__ constexpr int tier_cap_lg_val(int t) { return t == 0 ? 10 : (t == 1 ? 12 : (t == 2 ? 13 : 30)); }
-constexpr int64_t TIER_FLOPS0 = 4096;
+constexpr int64_t TIER_FLOPS0 = 8192;
 constexpr int64_t TIER_FLOPS1 = 65536;
 
 struct Summary {

@@ -81,7 +81,7 @@ struct mm_handle {
     Summary sum{};
     mm_stats_t stats{};
     // ---- tuning (mm_set_tuning) ----
-    long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;
+    long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;   // defaults: analyze.cuh
     int capc_lg = CAPC_LG, load_shift = 2;
     int rank_budget[3] = {6144, 24576, 49152};
     int auto_mca_nm = 0;
@@ -226,7 +226,7 @@ RankKernel pick_rank_unordered(int tier, int* gw) {
         case 0: *gw = 1; return k_push_rank<1, true, KIND, MSA, NUM>;
         case 1: *gw = 4; return k_push_rank<4, true, KIND, MSA, NUM>;
 #ifndef MM_RANK_T2_GW
-#define MM_RANK_T2_GW 16
+#define MM_RANK_T2_GW 8
 #endif
         case 2: *gw = MM_RANK_T2_GW; return k_push_rank<MM_RANK_T2_GW, true, KIND, MSA, NUM>;
         default: *gw = 32; return k_push_rank<32, false, KIND, MSA, NUM>;
