@@ -153,57 +153,26 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 sb = bsm.base[l] + a0;
                 if (KIND == 1) sa = bsm.av[l];
             }
-            // long portions: warp-wide chunks of CH products, software-pipelined
-            // one chunk ahead (across portion boundaries too), so the B loads
-            // of chunk c+1 are in flight while chunk c is probed
             unsigned longm = __ballot_sync(FULL, plen >= 32);
-            int nsrc = -1, nn0 = 0, nc = 0;
-            long long nb0 = 0, na0 = 0;
-            int32_t nx[U];
-            if (longm) {
-                nsrc = __ffs(longm) - 1;
+            while (longm) {
+                const int src = __ffs(longm) - 1;
                 longm &= longm - 1;
-                nb0 = shfl64(sb, nsrc);
-                nn0 = __shfl_sync(FULL, plen, nsrc);
-                na0 = KIND == 1 ? __shfl_sync(FULL, sa, nsrc) : 0;
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const int o = 32 * u + lane32;
-                    nx[u] = o < nn0 ? __ldg(p.b_idx + nb0 + o) : EMPTY_KEY;
-                }
-            }
-            while (nsrc >= 0) {
-                int32_t jj[U];
-                long long aa[U], ss[U];
-                const long long cb0 = nb0, ca0 = na0;
-                const int cc = nc;
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    jj[u] = nx[u];
-                    aa[u] = ca0;
-                    ss[u] = cb0 + cc + 32 * u + lane32;
-                }
-                nc += CH;
-                if (nc >= nn0) {
-                    nc = 0;
-                    if (longm) {
-                        nsrc = __ffs(longm) - 1;
-                        longm &= longm - 1;
-                        nb0 = shfl64(sb, nsrc);
-                        nn0 = __shfl_sync(FULL, plen, nsrc);
-                        na0 = KIND == 1 ? __shfl_sync(FULL, sa, nsrc) : 0;
-                    } else {
-                        nsrc = -1;
-                    }
-                }
-                if (nsrc >= 0) {
+                const long long b0 = shfl64(sb, src);
+                const int n0 = __shfl_sync(FULL, plen, src);
+                const long long a0 = KIND == 1 ? __shfl_sync(FULL, sa, src) : 0;
+                const int32_t* bp = p.b_idx + b0;
+                for (int c = 0; c < n0; c += CH) {
+                    int32_t jj[U];
+                    long long aa[U], ss[U];
 #pragma unroll
                     for (int u = 0; u < U; u++) {
-                        const int o = nc + 32 * u + lane32;
-                        nx[u] = o < nn0 ? __ldg(p.b_idx + nb0 + o) : EMPTY_KEY;
+                        const int o = c + 32 * u + lane32;
+                        jj[u] = o < n0 ? __ldg(bp + o) : EMPTY_KEY;
+                        aa[u] = a0;
+                        ss[u] = b0 + o;
                     }
+                    pr.template put_batch<U>(jj, aa, ss);
                 }
-                pr.template put_batch<U>(jj, aa, ss);
             }
             const int slen = plen < 32 ? plen : 0;
             const int sincl = warp_incl_scan(slen, lane32);
