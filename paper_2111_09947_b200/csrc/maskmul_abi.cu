@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,6 +32,15 @@ namespace {
 
 thread_local std::string g_last_error;
 thread_local long long g_launches = 0;   // kernels launched by this thread (profiling)
+
+bool debug_launches() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MM_DEBUG_LAUNCH");
+        on = e && *e && *e != '0';
+    }
+    return on == 1;
+}
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -322,6 +332,9 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
                 h->allocs.push_back(gslab);
             }
             ++g_launches;
+            if (debug_launches())
+                fprintf(stderr, "[mm] hash bin %d rows %d gw %d threads %d cap_lg %d smem %zu grid %d occ %d\n", b,
+                        cnt, gw, threads, cap_lg, smem, grid, occ);
             kern<<<grid, threads, smem, st>>>(h->prob, out, wk, h->row_cap_lg, cap_lg, gslab);
             CU(cudaGetLastError());
             continue;
@@ -353,6 +366,9 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
                 h->allocs.push_back(gslab);
             }
             ++g_launches;
+            if (debug_launches())
+                fprintf(stderr, "[mm] rank bin %d rows %d gw %d threads %d words %d nm %d smem %zu grid %d occ %d\n", b,
+                        cnt, gw, threads, words_max, nm_max, smem, grid, occ);
             kern<<<grid, threads, smem, st>>>(h->prob, out, wk, words_max, nm_max, gslab);
             CU(cudaGetLastError());
             continue;
