@@ -90,6 +90,7 @@ struct mm_handle {
     int bin_off[NBINS + 1] = {0};
     Summary sum{};
     mm_stats_t stats{};
+    int bound_flag = 0;
     // ---- tuning (mm_set_tuning) ----
     long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;   // defaults: analyze.cuh
     int capc_lg = CAPC_LG, load_shift = 2;
@@ -592,12 +593,19 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     o.out_f64 = h->out_f64;
     if ((rc = launch_bins(h, true, o))) return rc;
     mark(h, 3);
+    if (m > 0) {
+        // the bound assertion (multiply.py:390) rides on the nnz readback below
+        int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8);
+        ++g_launches;
+        k_check_bounds<<<grid, 256, 0, st>>>(m, h->row_nnz, h->bound_off, &h->d_summary->flag);
+    }
     if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st))) return rc;
     CU(cudaMemcpyAsync(&h->d_summary->total_nnz, h->c_row_ptr + m, sizeof(long long),
                        cudaMemcpyDeviceToDevice, st));
     if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
     h->total_nnz = h->h_summary->total_nnz;
     h->stats.evaluated_multiplies = (int64_t)h->h_summary->evaluated;
+    h->bound_flag = h->h_summary->flag;
     mark(h, 4);
     *out_nnz = h->total_nnz;
     h->active = true;
@@ -622,16 +630,15 @@ int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_value
             if (h->out_f64)
                 k_compact<double><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
                                                         (const double*)h->tmp_val, h->c_row_ptr,
-                                                        c_col_idx, (double*)c_values, flag);
+                                                        c_col_idx, (double*)c_values, nullptr);
             else
-        k_compact<long long><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
+                k_compact<long long><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
                                                            (const long long*)h->tmp_val, h->c_row_ptr,
-                                                           c_col_idx, (long long*)c_values, flag);
+                                                           c_col_idx, (long long*)c_values, nullptr);
             CU(cudaGetLastError());
         }
         mark(h, 5);
-        // the bound flag is checked lazily: read it with the stats below
-        if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) { release(h); return rc; }
+        // no sync: counters and the bound flag came back with the nnz readback
     } else {
         if ((rc = dalloc(h, &h->row_nnz2, m))) { release(h); return rc; }
         if (m > 0) CU(cudaMemsetAsync(h->row_nnz2, 0, m * sizeof(int64_t), st));
@@ -652,7 +659,7 @@ int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_value
         if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) { release(h); return rc; }
         h->stats.evaluated_multiplies = (int64_t)h->h_summary->evaluated;
     }
-    int bad = h->h_summary->flag;
+    int bad = h->plan.phases == 1 ? h->bound_flag : h->h_summary->flag;
     h->launches = g_launches - h->launch_base;
     h->stats.output_nnz = h->total_nnz;
     if (stats) *stats = h->stats;

@@ -76,8 +76,9 @@ __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* b
     const int lane = threadIdx.x & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = gtid; i < nrows; i += nthreads)
-        if (row_nnz[i] > bounds_off[i + 1] - bounds_off[i]) atomicExch(flag, 1);
+    if (flag)
+        for (int64_t i = gtid; i < nrows; i += nthreads)
+            if (row_nnz[i] > bounds_off[i + 1] - bounds_off[i]) atomicExch(flag, 1);
     const int64_t total = out_ptr[nrows];
     const int64_t warp = gtid >> 5;
     const int64_t nwarps = nthreads >> 5;
@@ -112,6 +113,13 @@ __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* b
             }
         }
     }
+}
+
+// 1P check: no row overran its slot range (multiply.py:390).
+__global__ void k_check_bounds(int64_t n, const int64_t* row_nnz, const int64_t* bounds_off, int* flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (row_nnz[i] > bounds_off[i + 1] - bounds_off[i]) atomicExch(flag, 1);
 }
 
 // 2P check: symbolic counts must equal the numeric row sizes (multiply.py:375).
