@@ -62,6 +62,60 @@ __device__ __forceinline__ int group_incl_scan(int v, int* total, int* s_warp, i
     }
 }
 
+// Offsets of one row (A and mask).
+struct RowInfo {
+    int64_t i, as, ae, ms, me;
+};
+
+// Dynamic row fetch for a group of GW warps.  Single-warp groups take 32 rows
+// per global atomic and preload the 32 rows' offsets, one per lane, so the
+// per-row fetch latency of small rows is paid once per 32 rows.
+template <int GW>
+struct RowFetcher {
+    int n = 0, q = 0;
+    int64_t li = 0, las = 0, lae = 0, lms = 0, lme = 0;
+    __device__ __forceinline__ bool next(const Prob& p, const Work& wk, int gt, int bar_id, int* s_row,
+                                         RowInfo& ri) {
+        const int lane = gt & 31;
+        if (GW == 1) {
+            if (q >= n) {
+                int b = 0;
+                if (lane == 0) b = atomicAdd(wk.cursor, 32);
+                b = __shfl_sync(FULL, b, 0);
+                if (b >= wk.count) return false;
+                n = wk.count - b < 32 ? wk.count - b : 32;
+                q = 0;
+                if (lane < n) {
+                    li = wk.rows[b + lane];
+                    las = p.a_ptr[li];
+                    lae = p.a_ptr[li + 1];
+                    lms = p.m_ptr[li];
+                    lme = p.m_ptr[li + 1];
+                }
+            }
+            ri.i = shfl64(li, q);
+            ri.as = shfl64(las, q);
+            ri.ae = shfl64(lae, q);
+            ri.ms = shfl64(lms, q);
+            ri.me = shfl64(lme, q);
+            q++;
+            return true;
+        } else {
+            if (gt == 0) *s_row = atomicAdd(wk.cursor, 1);
+            group_bar(bar_id, GW * 32);
+            const int r = *s_row;
+            group_bar(bar_id, GW * 32);
+            if (r >= wk.count) return false;
+            ri.i = wk.rows[r];
+            ri.as = p.a_ptr[ri.i];
+            ri.ae = p.a_ptr[ri.i + 1];
+            ri.ms = p.m_ptr[ri.i];
+            ri.me = p.m_ptr[ri.i + 1];
+            return true;
+        }
+    }
+};
+
 // Shared-memory staging of one batch of A entries: base of the B row (made
 // relative to the batch's product index), A value (int64 plus-times), and
 // the inclusive product end.  Bytes per group.

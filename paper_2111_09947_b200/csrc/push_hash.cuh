@@ -314,7 +314,7 @@ struct HashLocatorF64 {
 // The row processor.
 // ---------------------------------------------------------------------------
 template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
-__device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, int64_t i,
+__device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
                                          int cap_lg, int gt, int bar_id, int* s_warp,
                                          BatchSmem bsm, unsigned char* wq,
                                          unsigned long long& evaluated) {
@@ -323,8 +323,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     const int wg = gt >> 5;
     const int cap = 1 << cap_lg;
     const uint32_t cmask = (uint32_t)cap - 1;
-    const int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1];
-    const int64_t ms = p.m_ptr[i], me = p.m_ptr[i + 1];
+    const int64_t i = ri.i, as = ri.as, ae = ri.ae, ms = ri.ms, me = ri.me;
 
     // 1. clear the table
     for (int e = gt; e < cap; e += GT) {
@@ -503,16 +502,11 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
     Table<KIND> tb;
     tb.bind(base, cap_max);
     unsigned long long evaluated = 0;
-    for (;;) {
-        if (gt == 0) s_row[g] = atomicAdd(wk.cursor, 1);
-        group_bar(bar_id, GT);
-        int r = s_row[g];
-        group_bar(bar_id, GT);
-        if (r >= wk.count) break;
-        int64_t i = wk.rows[r];
-        hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, i, row_cap_lg[i], gt, bar_id,
-                                          s_warp + g * GW, bsm, wq, evaluated);
-    }
+    RowFetcher<GW> rf;
+    RowInfo ri;
+    while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
+        hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg[ri.i], gt, bar_id,
+                                                s_warp + g * GW, bsm, wq, evaluated);
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);
         if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);

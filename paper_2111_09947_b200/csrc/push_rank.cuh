@@ -212,12 +212,11 @@ __host__ __device__ constexpr size_t rank_region_bytes(bool msa, bool smem, int6
 template <int GW, int KIND, bool MSA, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned char* region, int nm_max,
                                          int words_max,
-                                         int64_t i, int gt, int bar_id, int* s_warp, BatchSmem bsm,
+                                         const RowInfo& ri, int gt, int bar_id, int* s_warp, BatchSmem bsm,
                                          unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
     const int lane = gt & 31;
-    const int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1];
-    const int64_t ms = p.m_ptr[i], me = p.m_ptr[i + 1];
+    const int64_t i = ri.i, as = ri.as, ae = ri.ae, ms = ri.ms, me = ri.me;
     const int nm = (int)(me - ms);
     RankSlots<KIND> sl;
     sl.val = KIND == 0 ? nullptr : (unsigned long long*)region;
@@ -359,15 +358,11 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
         uint32_t* bits = (uint32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
         for (int w = gt; w < words_max; w += GT) bits[w] = 0u;
     }
-    for (;;) {
-        if (gt == 0) s_row[g] = atomicAdd(wk.cursor, 1);
-        group_bar(bar_id, GT);
-        const int r = s_row[g];
-        group_bar(bar_id, GT);
-        if (r >= wk.count) break;
-        rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, words_max, wk.rows[r], gt, bar_id,
+    RowFetcher<GW> rf;
+    RowInfo ri;
+    while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
+        rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, words_max, ri, gt, bar_id,
                                                s_warp + g * GW, bsm, evaluated);
-    }
     if (NUMERIC) {
         const long long e = warp_sum_ll((long long)evaluated);
         if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);
