@@ -67,9 +67,13 @@ struct RowInfo {
     int64_t i, as, ae, ms, me;
 };
 
-// Dynamic row fetch for a group of GW warps.  Single-warp groups take 32 rows
-// per global atomic and preload the 32 rows' offsets, one per lane, so the
-// per-row fetch latency of small rows is paid once per 32 rows.
+// Dynamic row fetch for a group of GW warps.  Single-warp groups take
+// ROWS_PER_FETCH rows per global atomic and preload their offsets, one per
+// lane, so the fetch latency of small rows is paid once per batch (small
+// batches keep the tail balanced).
+#ifndef MM_ROWS_PER_FETCH
+#define MM_ROWS_PER_FETCH 4
+#endif
 template <int GW>
 struct RowFetcher {
     int n = 0, q = 0;
@@ -80,10 +84,10 @@ struct RowFetcher {
         if (GW == 1) {
             if (q >= n) {
                 int b = 0;
-                if (lane == 0) b = atomicAdd(wk.cursor, 32);
+                if (lane == 0) b = atomicAdd(wk.cursor, MM_ROWS_PER_FETCH);
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= wk.count) return false;
-                n = wk.count - b < 32 ? wk.count - b : 32;
+                n = wk.count - b < MM_ROWS_PER_FETCH ? wk.count - b : MM_ROWS_PER_FETCH;
                 q = 0;
                 if (lane < n) {
                     li = wk.rows[b + lane];
