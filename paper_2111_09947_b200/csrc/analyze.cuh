@@ -30,8 +30,10 @@ enum Bin : int {
     BIN_MCA0 = 27,    // + tier
     BIN_HEAP0 = 31,   // + tier
     BIN_SINGLE = 35,  // one A entry: filtered, scaled copy of B_k (auto)
-    NBINS = 36
+    BIN_MSAS0 = 36,   // + tier (0..2): MSA with a sparse two-level window bitmap
+    NBINS = 39
 };
+__host__ __device__ constexpr bool is_msas_bin(int b) { return b >= BIN_MSAS0 && b < BIN_MSAS0 + 3; }
 __host__ __device__ constexpr bool is_msa_bin(int b) { return b >= BIN_MSA0 && b < BIN_MSA0 + 4; }
 __host__ __device__ constexpr bool is_mca_bin(int b) { return b >= BIN_MCA0 && b < BIN_MCA0 + 4; }
 __host__ __device__ constexpr bool is_heap_bin(int b) { return b >= BIN_HEAP0 && b < BIN_HEAP0 + 4; }
@@ -92,6 +94,14 @@ __device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
 __host__ __device__ constexpr int64_t msa_bytes(int64_t words, int64_t nm, int kind) {
     return 6 * words + (kind == 0 ? 4 : 12) * nm;   // shared tiers: u16 rank prefix
 }
+// sparse window: u16 directory per 1024 columns + 32 words (+u16 prefixes) per touched block
+__host__ __device__ constexpr int64_t msas_dir(int64_t words) { return ((words - 1) >> 5) + 1; }
+__host__ __device__ constexpr int64_t msas_blocks(int64_t words, int64_t nm) {
+    return nm < msas_dir(words) ? nm : msas_dir(words);
+}
+__host__ __device__ constexpr int64_t msas_bytes(int64_t words, int64_t nm, int kind) {
+    return 2 * msas_dir(words) + 192 * msas_blocks(words, nm) + (kind == 0 ? 4 : 12) * nm;
+}
 __host__ __device__ constexpr int64_t mca_bytes(int64_t nm, int kind) {
     return (kind == 0 ? 8 : 16) * nm;
 }
@@ -100,8 +110,9 @@ __host__ __device__ constexpr int64_t mca_bytes(int64_t nm, int kind) {
 // words = 32-column words spanned by the mask row (MSA window).
 __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na, int64_t nm,
                                             int64_t flops, int64_t ncols, int64_t pull_cols,
-                                            int64_t words, int* cap_lg_out) {
+                                            int64_t words, int* cap_lg_out, int64_t* aux_out) {
     *cap_lg_out = 0;
+    *aux_out = words;
     if (flops == 0 || (!ap.comp && nm == 0)) return BIN_EMPTY;
     const int kind = ap.pair ? 0 : (ap.ordered ? 2 : 1);
     const int tf = flops <= ap.tier_flops0 ? 0 : (flops <= ap.tier_flops1 ? 1 : 2);
@@ -119,6 +130,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             if (ap.has_bt && pull < push) fam = FAM_PULL;
             // push: the bitmap accumulator when the mask window is compact
             else if (msa_bytes(words, nm, kind) <= ap.rank_budget[tr]) fam = FAM_MSA;
+            else if (msas_bytes(words, nm, kind) <= ap.rank_budget[tr] && nm < 65536) fam = FAM_MSA;
             else if (tr == 0 && nm <= ap.auto_mca_nm) fam = FAM_MCA;
         }
     }
@@ -131,6 +143,13 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             return BIN_HEAP0 + (bytes <= ap.rank_budget[0] ? 0 : 1);
         }
         if (na <= 32) return BIN_HEAP0 + 2;
+    }
+    if (!ap.comp && fam == FAM_MSA && msa_bytes(words, nm, kind) > ap.rank_budget[tr] &&
+        msas_bytes(words, nm, kind) <= ap.rank_budget[tr] && nm < 65536) {
+        // narrow mask over a wide window: sparse two-level bitmap
+        *cap_lg_out = (int)msas_blocks(words, nm);   // per-bin maximum of touched blocks
+        *aux_out = msas_dir(words);                   // per-bin maximum directory length
+        return BIN_MSAS0 + tr;
     }
     if (!ap.comp && (fam == FAM_MSA || fam == FAM_MCA)) {
         const int64_t bytes = fam == FAM_MSA ? msa_bytes(words, nm, kind) : mca_bytes(nm, kind);
@@ -269,8 +288,8 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
                 my_bound += bd;
             }
             int cap_lg;
-            const int64_t words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
-            b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg);
+            int64_t words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
+            b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg, &words);
             row_bin[i] = (uint8_t)b;
             row_cap_lg[i] = (int8_t)cap_lg;
             atomicAdd(&s_bflops[b], (unsigned long long)f);

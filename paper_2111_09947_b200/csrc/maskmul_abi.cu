@@ -24,6 +24,7 @@
 #include "push_rank.cuh"
 #include "push_heap.cuh"
 #include "push_single.cuh"
+#include "push_msa_sparse.cuh"
 #include "scan_compact.cuh"
 
 using namespace mm;
@@ -405,6 +406,42 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             }
             ++g_launches;
             kern<<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max, h->plan.n_inspect, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
+        if (is_msas_bin(b)) {
+            const int tier = b - BIN_MSAS0;
+            const int kind = numeric ? h->kind : 0;
+            void (*kern)(Prob, Out, Work, int, int, int) = nullptr;
+            int gw = kind == 2 ? 1 : (tier == 0 ? 1 : (tier == 1 ? 4 : 8));
+            if (!numeric || kind == 0) {
+                if (gw == 1) kern = numeric ? k_push_msas<1, 0, true> : k_push_msas<1, 0, false>;
+                else if (gw == 4) kern = numeric ? k_push_msas<4, 0, true> : k_push_msas<4, 0, false>;
+                else kern = numeric ? k_push_msas<8, 0, true> : k_push_msas<8, 0, false>;
+            } else if (kind == 1) {
+                kern = gw == 1 ? k_push_msas<1, 1, true> : (gw == 4 ? k_push_msas<4, 1, true> : k_push_msas<8, 1, true>);
+            } else {
+                kern = k_push_msas<1, 2, true>;
+            }
+            const int groups = 256 / (32 * gw);
+            const int d_max = std::max(h->sum.bin_words[b], 1);
+            const int blk_max = std::max(h->sum.bin_cap_lg[b], 1);
+            const int nm_max = std::max(h->sum.bin_nmmax[b], 1);
+            size_t rb = (size_t)(kind == 0 ? 0 : 8) * nm_max + 4 * (size_t)nm_max + 2 * (size_t)((d_max + 1) & ~1) +
+                        192 * (size_t)blk_max;
+            rb = (rb + 15) & ~(size_t)15;
+            const size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            const size_t smem = groups * (rb + batch);
+            if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "sparse MSA region exceeds shared memory");
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            const int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
+            if (debug_launches())
+                fprintf(stderr, "[mm] sparse-msa bin %d rows %d gw %d dir %d blk %d nm %d smem %zu grid %d occ %d\n",
+                        b, cnt, gw, d_max, blk_max, nm_max, smem, grid, occ);
+            ++g_launches;
+            kern<<<grid, 256, smem, st>>>(h->prob, out, wk, d_max, blk_max, nm_max);
             CU(cudaGetLastError());
             continue;
         }
