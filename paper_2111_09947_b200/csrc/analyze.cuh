@@ -130,7 +130,6 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             if (ap.has_bt && pull < push) fam = FAM_PULL;
             // push: the bitmap accumulator when the mask window is compact
             else if (msa_bytes(words, nm, kind) <= ap.rank_budget[tr]) fam = FAM_MSA;
-            else if (msas_bytes(words, nm, kind) <= ap.rank_budget[tr] && nm < 65536) fam = FAM_MSA;
             else if (tr == 0 && nm <= ap.auto_mca_nm) fam = FAM_MCA;
         }
     }
