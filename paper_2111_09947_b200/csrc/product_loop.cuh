@@ -256,11 +256,17 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
     }
 }
 
-// Ordered float64 accumulation for one warp: A entries in ascending order
-// (= ascending k, the reference's sum order, _kernels.py:48-65), lanes over
-// the entries of B_k; within one k no two lanes share a column, and
-// __syncwarp orders consecutive k, so every slot folds its products exactly
-// like the reference (first product stored, then added: _kernels.py:58-65).
+// Ordered float64 accumulation for one warp.  The reference folds a slot's
+// products in ascending k, the first product stored rather than added to 0.0
+// (_kernels.py:48-65); every GPU float64 path keeps that order, so results are
+// bit-identical to the reference's MSA/Hash/MCA/Inner.
+//
+// The warp walks the row's product space flattened in (k, s) order, 32
+// consecutive products per window (owner A entry of each lane found by a
+// shuffle binary search), so short B rows do not idle lanes.  Windows are
+// processed in order; inside a window, lanes whose products land on the same
+// slot (two k's hitting one column) fold one after another in lane order
+// (__match_any_sync ranks them), everyone else folds at once.
 // loc.locate(j) -> slot or -1 (masked out); loc.fold(slot, prod); loc.mark(slot).
 template <bool NUMERIC, class LOC>
 __device__ __forceinline__ unsigned ordered_products_f64(const Prob& p, LOC& loc, int64_t as, int64_t ae,
@@ -270,24 +276,39 @@ __device__ __forceinline__ unsigned ordered_products_f64(const Prob& p, LOC& loc
     unsigned evaluated = 0;
     for (int64_t tb0 = as; tb0 < ae; tb0 += 32) {
         const int64_t t = tb0 + lane;
-        int64_t bs = 0, be = 0;
+        int64_t bs = 0;
+        int len = 0;
         double av = 0.0;
         if (t < ae) {
             const int32_t k = p.a_idx[t];
             bs = p.b_ptr[k];
-            be = p.b_ptr[k + 1];
+            len = (int)(p.b_ptr[k + 1] - bs);
             av = av_p[t];
         }
-        const int nb = (int)min((int64_t)32, ae - tb0);
-        for (int q = 0; q < nb; q++) {
-            const int64_t s0 = shfl64(bs, q), s1 = shfl64(be, q);
-            const double a = __shfl_sync(FULL, av, q);
-            for (int64_t s = s0 + lane; s < s1; s += 32) {
-                const int h = loc.locate(p.b_idx[s]);
-                if (h < 0) continue;
-                evaluated++;
-                if (NUMERIC) loc.fold(h, a * bv_p[s]);
-                else loc.mark(h);
+        const int incl = warp_incl_scan(len, lane);
+        const int tot = __shfl_sync(FULL, incl, 31);
+        const int excl = incl - len;
+        for (int w0 = 0; w0 < tot; w0 += 32) {
+            const int q = w0 + lane;
+            const int own = owner_of(incl, q < tot ? q : tot - 1);
+            const int64_t s = shfl64(bs, own) + (q - __shfl_sync(FULL, excl, own));
+            const double a = __shfl_sync(FULL, av, own);
+            const int h = q < tot ? loc.locate(p.b_idx[s]) : -1;
+            const bool hit = h >= 0;
+            evaluated += hit;
+            const unsigned hm = __ballot_sync(FULL, hit);
+            if (!hm) continue;
+            if (NUMERIC) {
+                const double prod = hit ? a * bv_p[s] : 0.0;
+                const unsigned same = __match_any_sync(FULL, hit ? h : -2 - lane);
+                const int myrank = __popc(same & lanemask_lt());
+                const int rounds = __reduce_max_sync(FULL, hit ? myrank : 0);
+                for (int r = 0; r <= rounds; r++) {
+                    if (hit && myrank == r) loc.fold(h, prod);
+                    __syncwarp();
+                }
+            } else if (hit) {
+                loc.mark(h);
             }
             __syncwarp();
         }
