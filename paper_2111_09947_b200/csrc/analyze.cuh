@@ -128,6 +128,9 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             int64_t push = 16 * na + flops * w;
             int64_t pull = 16 * nm + (nm * na + pull_cols) * w;
             if (ap.has_bt && pull < push) fam = FAM_PULL;
+            // ordered float64 rows (one warp, k order): the rank search beats
+            // both the bitmap and the hash for short mask rows
+            else if (ap.ordered && nm <= 512) fam = FAM_MCA;
             // push: the bitmap accumulator when the mask window is compact
             else if (msa_bytes(words, nm, kind) <= ap.rank_budget[tr]) fam = FAM_MSA;
             else if (tr == 0 && nm <= ap.auto_mca_nm) fam = FAM_MCA;
