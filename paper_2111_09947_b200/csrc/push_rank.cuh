@@ -336,7 +336,10 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
 // Groups of GW warps fetch rows of one bin.  SMEM: the per-group region lives
 // in dynamic shared memory, otherwise in one global slab per group (tier 3).
 template <int GW, bool SMEM, int KIND, bool MSA, bool NUMERIC>
-__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256))
+#ifndef MM_RANK_MINB
+#define MM_RANK_MINB 1
+#endif
+__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256), GW <= 8 ? MM_RANK_MINB : 1)
 k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gslab) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_row[16];
