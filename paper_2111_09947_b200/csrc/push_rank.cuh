@@ -123,6 +123,7 @@ struct MsaProber {
                 : "r"(off[u]), "r"(span), "r"(bits_s + w4[u]));
 #pragma unroll
         for (int u = 0; u < U; u++) hit[u] = (word[u] >> (off[u] & 31u)) & 1u;
+#ifndef MM_EXPERIMENT_NORANK
 #pragma unroll
         for (int u = 0; u < U; u++)
             asm volatile(
@@ -131,9 +132,14 @@ struct MsaProber {
                 "@ph ld.shared.u16 %0, [%2];\n\t}"
                 : "+r"(pre[u])
                 : "r"(hit[u]), "r"(pre_s + (w4[u] >> 1)));
+#endif
 #pragma unroll
         for (int u = 0; u < U; u++) {
+#ifdef MM_EXPERIMENT_NORANK
+            const uint32_t rank = 0;   // profiling-only build: hit path without the rank
+#else
             const uint32_t rank = pre[u] + __popc(word[u] & ((1u << (off[u] & 31u)) - 1u));
+#endif
             evaluated += hit[u];
             if (KIND == 0) {
                 if (NUMERIC)
