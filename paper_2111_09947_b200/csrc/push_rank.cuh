@@ -68,6 +68,23 @@ struct MsaBits {
     }
 };
 
+// Shared tiers pack 16 columns and the 16-bit mask rank of the word's first
+// set bit into one 32-bit word: (rank << 16) | bits.  One shared load gives
+// both the membership bit and the rank base.
+struct MsaPacked {
+    const uint32_t* words;
+    int32_t lo;
+    uint32_t span;
+    __device__ __forceinline__ int rank(int32_t j) const {
+        const uint32_t off = (uint32_t)(j - lo);
+        if (off > span) return -1;
+        const uint32_t word = words[off >> 4];
+        const uint32_t b = off & 15u;
+        if (!((word >> b) & 1u)) return -1;
+        return (int)(word >> 16) + __popc(word & ((1u << b) - 1u));
+    }
+};
+
 // --- MCA rank search -------------------------------------------------------
 struct McaRow {
     const int32_t* m;   // mask row (shared)
@@ -89,7 +106,7 @@ struct McaRow {
 // B value of a product is loaded only when its column survives the mask).
 template <int KIND, bool NUMERIC>
 struct MsaProber {
-    uint32_t bits_s, pre_s, cnt_s, val_s;
+    uint32_t bits_s, cnt_s, val_s;     // bits_s: packed (rank << 16 | 16 column bits) words
     int32_t lo;
     uint32_t span;
     const void* b_val;
@@ -105,13 +122,11 @@ struct MsaProber {
         for (int u = 0; u < U; u++) evaluated += (j[u] != EMPTY_KEY);
         return;
 #endif
-        uint32_t off[U], w4[U], word[U], pre[U], hit[U];   // pre: u16 rank prefix per word
+        uint32_t off[U], word[U], hit[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             off[u] = (uint32_t)(j[u] - lo);      // EMPTY_KEY -> off > span
-            w4[u] = (off[u] >> 5) << 2;
             word[u] = 0u;
-            pre[u] = 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
@@ -120,26 +135,12 @@ struct MsaProber {
                 "setp.le.u32 pin, %1, %2;\n\t"
                 "@pin ld.shared.u32 %0, [%3];\n\t}"
                 : "+r"(word[u])
-                : "r"(off[u]), "r"(span), "r"(bits_s + w4[u]));
+                : "r"(off[u]), "r"(span), "r"(bits_s + ((off[u] >> 4) << 2)));
 #pragma unroll
-        for (int u = 0; u < U; u++) hit[u] = (word[u] >> (off[u] & 31u)) & 1u;
-#ifndef MM_EXPERIMENT_NORANK
-#pragma unroll
-        for (int u = 0; u < U; u++)
-            asm volatile(
-                "{\n\t.reg .pred ph;\n\t"
-                "setp.ne.u32 ph, %1, 0;\n\t"
-                "@ph ld.shared.u16 %0, [%2];\n\t}"
-                : "+r"(pre[u])
-                : "r"(hit[u]), "r"(pre_s + (w4[u] >> 1)));
-#endif
+        for (int u = 0; u < U; u++) hit[u] = (word[u] >> (off[u] & 15u)) & 1u;
 #pragma unroll
         for (int u = 0; u < U; u++) {
-#ifdef MM_EXPERIMENT_NORANK
-            const uint32_t rank = 0;   // profiling-only build: hit path without the rank
-#else
-            const uint32_t rank = pre[u] + __popc(word[u] & ((1u << (off[u] & 31u)) - 1u));
-#endif
+            const uint32_t rank = (word[u] >> 16) + __popc(word[u] & ((1u << (off[u] & 15u)) - 1u));
             evaluated += hit[u];
             if (KIND == 0) {
                 if (NUMERIC)
@@ -208,11 +209,13 @@ struct RankLocatorF64 {
 };
 
 // Per-group region: [val: 8*NM if KIND != 0][cnt: 4*NM]
-//   MSA: [bits 4*W][pre: 2*W (u16, shared tiers) or 4*W (global tier)]   MCA: [mask 4*NM]
+//   MSA shared tiers: [packed words 4*(2W)]  (16 columns + 16-bit rank prefix each)
+//   MSA global tier:  [bits 4*W][pre 4*W]    MCA: [mask 4*NM]
+// W = 32-column words spanned by the mask window.
 template <int KIND>
 __host__ __device__ constexpr size_t rank_region_bytes(bool msa, bool smem, int64_t words, int64_t nm) {
     return (size_t)(KIND == 0 ? 0 : 8) * nm + 4 * (size_t)nm +
-           (msa ? (smem ? 6 : 8) * (size_t)((words + 1) & ~1ll) : 4 * (size_t)nm);
+           (msa ? 8 * (size_t)((words + 1) & ~1ll) : 4 * (size_t)nm);
 }
 
 template <int GW, int KIND, bool MSA, bool NUMERIC, bool SMEM>
@@ -230,9 +233,8 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     unsigned char* aux = (unsigned char*)(sl.cnt + nm_max);
     const int32_t lo = p.m_idx[ms];
     const int32_t hi = p.m_idx[me - 1];
-    using PreT = typename std::conditional<SMEM, uint16_t, int32_t>::type;
     uint32_t* bits = (uint32_t*)aux;          // all-zero on entry (cleared by the previous row)
-    PreT* pre = (PreT*)(aux + 4 * (size_t)((words_max + 1) & ~1));
+    int32_t* pre = (int32_t*)(aux + 4 * (size_t)((words_max + 1) & ~1));   // global tier only
     int32_t* mrow = (int32_t*)aux;
 
     // 1. clear slots, 2. mark the mask row
@@ -243,11 +245,16 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     group_bar(bar_id, GT);
     for (int r = gt; r < nm; r += GT) {
         const int32_t j = p.m_idx[ms + r];
-        if (MSA) {
+        if (MSA && SMEM) {
+            const uint32_t off = (uint32_t)(j - lo);
+            const uint32_t w = off >> 4;
+            const bool first = r == 0 || (((uint32_t)(p.m_idx[ms + r - 1] - lo)) >> 4) != w;
+            atomicOr(bits + w, (1u << (off & 15u)) | (first ? (uint32_t)r << 16 : 0u));
+        } else if (MSA) {
             const uint32_t off = (uint32_t)(j - lo);
             const uint32_t w = off >> 5;
             atomicOr(bits + w, 1u << (off & 31u));
-            if (r == 0 || (((uint32_t)(p.m_idx[ms + r - 1] - lo)) >> 5) != w) pre[w] = (PreT)r;
+            if (r == 0 || (((uint32_t)(p.m_idx[ms + r - 1] - lo)) >> 5) != w) pre[w] = r;
         } else {
             mrow[r] = j;
         }
@@ -256,19 +263,25 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
 
     // 3. products
     if (MSA) {
-        MsaBits<PreT> rb{bits, pre, lo, (uint32_t)(hi - lo)};
         if (KIND == 2) {
-            RankLocatorF64<MsaBits<PreT>> loc{rb, sl.cnt, (double*)sl.val};
-            evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+            if (SMEM) {
+                MsaPacked rb{bits, lo, (uint32_t)(hi - lo)};
+                RankLocatorF64<MsaPacked> loc{rb, sl.cnt, (double*)sl.val};
+                evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+            } else {
+                MsaBits<int32_t> rb{bits, pre, lo, (uint32_t)(hi - lo)};
+                RankLocatorF64<MsaBits<int32_t>> loc{rb, sl.cnt, (double*)sl.val};
+                evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+            }
         } else {
           if (!SMEM) {
-            RankProber<KIND, NUMERIC, MsaBits<PreT>> pr{rb, sl, p.b_val, 0u};
+            MsaBits<int32_t> rb{bits, pre, lo, (uint32_t)(hi - lo)};
+            RankProber<KIND, NUMERIC, MsaBits<int32_t>> pr{rb, sl, p.b_val, 0u};
             flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
             evaluated += pr.evaluated;
           } else {
             MsaProber<KIND, NUMERIC> pr;
             pr.bits_s = (uint32_t)__cvta_generic_to_shared(bits);
-            pr.pre_s = (uint32_t)__cvta_generic_to_shared(pre);
             pr.cnt_s = (uint32_t)__cvta_generic_to_shared(sl.cnt);
             pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(sl.val);
             pr.lo = lo;
@@ -335,7 +348,7 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     if (gt == 0) o.row_nnz[i] = total;
     // 5. leave the bitmap all-zero for the next row (only the touched words)
     if (MSA)
-        for (int r = gt; r < nm; r += GT) bits[((uint32_t)(p.m_idx[ms + r] - lo)) >> 5] = 0u;
+        for (int r = gt; r < nm; r += GT) bits[((uint32_t)(p.m_idx[ms + r] - lo)) >> (SMEM ? 4 : 5)] = 0u;
     group_bar(bar_id, GT);
 }
 
@@ -365,7 +378,7 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     unsigned long long evaluated = 0;
     if (MSA) {
         uint32_t* bits = (uint32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
-        for (int w = gt; w < words_max; w += GT) bits[w] = 0u;
+        for (int w = gt; w < (SMEM ? 2 : 1) * words_max; w += GT) bits[w] = 0u;
     }
     RowFetcher<GW> rf;
     RowInfo ri;
