@@ -92,7 +92,7 @@ __device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
 
 // Shared-memory bytes per row of the rank-slot accumulators.
 __host__ __device__ constexpr int64_t msa_bytes(int64_t words, int64_t nm, int kind) {
-    return 8 * words + (kind == 0 ? 4 : 12) * nm;   // shared tiers: 16 columns + 16-bit rank per word
+    return 8 * words + 16 + (kind == 0 ? 4 : 12) * nm;   // shared tiers: 16 columns + 16-bit rank per word
 }
 // sparse window: u16 directory per 1024 columns + 32 words (+u16 prefixes) per touched block
 __host__ __device__ constexpr int64_t msas_dir(int64_t words) { return ((words - 1) >> 5) + 1; }

@@ -352,8 +352,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             const int groups = threads / (32 * gw);
             const int words_max = std::max(h->sum.bin_words[b], 1);
             const int nm_max = std::max(h->sum.bin_nmmax[b], 1);
-            size_t rb = (size_t)(kind == 0 ? 0 : 8) * nm_max + 4 * (size_t)nm_max +
-                        (msa ? 8 * (size_t)((words_max + 1) & ~1) : 4 * (size_t)nm_max);
+            size_t rb = rank_region_bytes_rt(kind, msa, words_max, nm_max);
             rb = (rb + 15) & ~(size_t)15;
             const size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
             const size_t smem = (smem_region ? groups * rb : 0) + groups * batch;

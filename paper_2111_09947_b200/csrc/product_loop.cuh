@@ -219,7 +219,20 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 const int n0 = __shfl_sync(FULL, plen, src);
                 const long long a0 = KIND == 1 ? __shfl_sync(FULL, sa, src) : 0;
                 const int32_t* bp = p.b_idx + b0;
-                for (int c = 0; c < n0; c += CH) {
+                int c = 0;
+                for (; c + CH <= n0; c += CH) {   // full chunks: no bounds predicates
+                    int32_t jj[U];
+                    long long aa[U], ss[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int o = c + 32 * u + lane32;
+                        jj[u] = __ldg(bp + o);
+                        aa[u] = a0;
+                        ss[u] = b0 + o;
+                    }
+                    pr.template put_batch<U>(jj, aa, ss);
+                }
+                if (c < n0) {
                     int32_t jj[U];
                     long long aa[U], ss[U];
 #pragma unroll

@@ -107,8 +107,8 @@ struct McaRow {
 template <int KIND, bool NUMERIC>
 struct MsaProber {
     uint32_t bits_s, cnt_s, val_s;     // bits_s: packed (rank << 16 | 16 column bits) words
-    int32_t lo;
-    uint32_t span;
+    int32_t lo;                        // window start, a multiple of 16
+    uint32_t guard;                    // offset of the all-zero guard word (multiple of 16)
     const void* b_val;
     unsigned evaluated;
     // U products at once, stage by stage, so the shared loads of the U
@@ -122,47 +122,51 @@ struct MsaProber {
         for (int u = 0; u < U; u++) evaluated += (j[u] != EMPTY_KEY);
         return;
 #endif
-        uint32_t off[U], word[U], hit[U];
+        // word = (rank of the group's first mask column << 16) | column bits.
+        // t = word << (31 - c) moves column c's bit to the sign and drops both
+        // the columns above c and the rank half, so hit = (t < 0) and the slot
+        // is rank + popc(t) - 1 (the -1 is folded into the slot base).
+        // Offsets outside the window (and EMPTY_KEY) clamp onto the guard word.
+        uint32_t word[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            off[u] = (uint32_t)(j[u] - lo);      // EMPTY_KEY -> off > span
-            word[u] = 0u;
+            const uint32_t off = min((uint32_t)(j[u] - lo), guard);
+            uint32_t addr;   // bits_s + 4 * (off >> 4) as SHF + LEA (ptxas otherwise emits SHF, LOP3, IADD)
+            asm("{\n\t.reg .u32 q;\n\tshr.u32 q, %1, 4;\n\tmad.lo.u32 %0, q, 4, %2;\n\t}"
+                : "=r"(addr) : "r"(off), "r"(bits_s));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(word[u]) : "r"(addr));
         }
 #pragma unroll
-        for (int u = 0; u < U; u++)
-            asm volatile(
-                "{\n\t.reg .pred pin;\n\t"
-                "setp.le.u32 pin, %1, %2;\n\t"
-                "@pin ld.shared.u32 %0, [%3];\n\t}"
-                : "+r"(word[u])
-                : "r"(off[u]), "r"(span), "r"(bits_s + ((off[u] >> 4) << 2)));
-#pragma unroll
-        for (int u = 0; u < U; u++) hit[u] = (word[u] >> (off[u] & 15u)) & 1u;
-#pragma unroll
         for (int u = 0; u < U; u++) {
-            const uint32_t rank = (word[u] >> 16) + __popc(word[u] & ((1u << (off[u] & 15u)) - 1u));
-            evaluated += hit[u];
+            // shift 31 - (j & 15) = (~j | 16) mod 32: one LOP3 + a wrapping funnel shift
+            uint32_t t;
+            asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(t) : "r"(0u), "r"(word[u]), "r"(~(uint32_t)j[u] | 16u));
+            const uint32_t slot = (word[u] >> 16) + __popc(t);     // rank + 1
+            const bool hit = (int32_t)t < 0;
             if (KIND == 0) {
+                // plus-pair: the evaluated count is the sum of the slot counts,
+                // taken when the row is gathered
                 if (NUMERIC)
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
-                        "setp.ne.u32 ph, %0, 0;\n\t"
-                        "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"(hit[u]),
-                        "r"(cnt_s + (rank << 2))
+                        "setp.lt.s32 ph, %0, 0;\n\t"
+                        "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"(t),
+                        "r"(cnt_s - 4u + (slot << 2))
                         : "memory");
                 else
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
-                        "setp.ne.u32 ph, %0, 0;\n\t"
-                        "@ph st.shared.u32 [%1], 1;\n\t}" ::"r"(hit[u]),
-                        "r"(cnt_s + (rank << 2))
+                        "setp.lt.s32 ph, %0, 0;\n\t"
+                        "@ph st.shared.u32 [%1], 1;\n\t}" ::"r"(t),
+                        "r"(cnt_s - 4u + (slot << 2))
                         : "memory");
-            } else if (hit[u]) {
+            } else if (hit) {
+                evaluated++;
                 if (NUMERIC) {
                     const long long prod = a[u] * ((const long long*)b_val)[s[u]];
-                    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(val_s + (rank << 3)), "l"(prod) : "memory");
+                    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(val_s - 8u + (slot << 3)), "l"(prod) : "memory");
                 }
-                asm volatile("st.shared.u32 [%0], 1;" ::"r"(cnt_s + (rank << 2)) : "memory");
+                asm volatile("st.shared.u32 [%0], 1;" ::"r"(cnt_s - 4u + (slot << 2)) : "memory");
             }
         }
     }
@@ -209,14 +213,19 @@ struct RankLocatorF64 {
 };
 
 // Per-group region: [val: 8*NM if KIND != 0][cnt: 4*NM]
-//   MSA shared tiers: [packed words 4*(2W)]  (16 columns + 16-bit rank prefix each)
-//   MSA global tier:  [bits 4*W][pre 4*W]    MCA: [mask 4*NM]
-// W = 32-column words spanned by the mask window.
-template <int KIND>
-__host__ __device__ constexpr size_t rank_region_bytes(bool msa, bool smem, int64_t words, int64_t nm) {
-    return (size_t)(KIND == 0 ? 0 : 8) * nm + 4 * (size_t)nm +
-           (msa ? 8 * (size_t)((words + 1) & ~1ll) : 4 * (size_t)nm);
+//   MSA shared tiers: [packed words 4*(2W' + 4)]  (16 columns + 16-bit rank each;
+//                      window start aligned down to 16 columns, plus an all-zero guard word)
+//   MSA global tier:  [bits 4*W'][pre 4*W' + 16]   MCA: [mask 4*NM]
+// W = 32-column words spanned by the mask window, W' = W rounded up to even.
+__host__ __device__ constexpr size_t rank_region_bytes_rt(int kind, bool msa, int64_t words, int64_t nm) {
+    return (size_t)(kind == 0 ? 0 : 8) * nm + 4 * (size_t)nm +
+           (msa ? 8 * (size_t)(((words + 1) & ~1ll) + 2) : 4 * (size_t)nm);
 }
+template <int KIND>
+__host__ __device__ constexpr size_t rank_region_bytes(bool msa, bool, int64_t words, int64_t nm) {
+    return rank_region_bytes_rt(KIND, msa, words, nm);
+}
+__host__ __device__ constexpr int msa_words16(int words_max) { return 2 * (((words_max + 1) & ~1) + 2); }
 
 template <int GW, int KIND, bool MSA, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned char* region, int nm_max,
@@ -231,10 +240,10 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     sl.val = KIND == 0 ? nullptr : (unsigned long long*)region;
     sl.cnt = (int32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max));
     unsigned char* aux = (unsigned char*)(sl.cnt + nm_max);
-    const int32_t lo = p.m_idx[ms];
+    const int32_t lo = MSA && SMEM ? p.m_idx[ms] & ~15 : p.m_idx[ms];
     const int32_t hi = p.m_idx[me - 1];
     uint32_t* bits = (uint32_t*)aux;          // all-zero on entry (cleared by the previous row)
-    int32_t* pre = (int32_t*)(aux + 4 * (size_t)((words_max + 1) & ~1));   // global tier only
+    int32_t* pre = (int32_t*)(aux + 4 * (size_t)(((words_max + 1) & ~1) + 2));   // global tier only
     int32_t* mrow = (int32_t*)aux;
 
     // 1. clear slots, 2. mark the mask row
@@ -285,7 +294,7 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
             pr.cnt_s = (uint32_t)__cvta_generic_to_shared(sl.cnt);
             pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(sl.val);
             pr.lo = lo;
-            pr.span = (uint32_t)(hi - lo);
+            pr.guard = (((uint32_t)(hi - lo) >> 4) + 1) << 4;
             pr.b_val = p.b_val;
             pr.evaluated = 0u;
             flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
@@ -312,7 +321,10 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     const int wg = gt >> 5;
     const int r_lo = (int)(((long long)nm * wg) / GW), r_hi = (int)(((long long)nm * (wg + 1)) / GW);
     int mine = 0;
-    for (int r = r_lo + lane; r < r_hi; r += 32) mine += sl.cnt[r] > 0;
+    for (int r = r_lo + lane; r < r_hi; r += 32) {
+        mine += sl.cnt[r] > 0;
+        if (MSA && SMEM && KIND == 0 && NUMERIC) evaluated += (unsigned)sl.cnt[r];
+    }
     mine = (int)warp_sum_ll(mine);
     int before = 0, total = mine;
     if (GW > 1) {
@@ -378,7 +390,7 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     unsigned long long evaluated = 0;
     if (MSA) {
         uint32_t* bits = (uint32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
-        for (int w = gt; w < (SMEM ? 2 : 1) * words_max; w += GT) bits[w] = 0u;
+        for (int w = gt; w < (SMEM ? msa_words16(words_max) : words_max); w += GT) bits[w] = 0u;
     }
     RowFetcher<GW> rf;
     RowInfo ri;
