@@ -57,8 +57,9 @@ __device__ __forceinline__ int ceil_log2_i64(int64_t x) {
 }
 
 // Fibonacci hash of a column index into a 2^lg table (lg >= 1).
+constexpr uint32_t FIB_MULT = 0x9E3779B1u;
 __device__ __forceinline__ uint32_t fib_hash(int32_t j, int lg) {
-    return ((uint32_t)j * 0x9E3779B1u) >> (32 - lg);
+    return ((uint32_t)j * FIB_MULT) >> (32 - lg);
 }
 
 // Named barrier for a group of `nthreads` (multiple of 32) threads; id 1..15.

@@ -58,8 +58,9 @@ struct Table {
 
 // Find the slot of key j (present or absent).  Returns slot index whose key is
 // j, or the EMPTY slot where the probe sequence ended (negated - 1).
-__device__ __forceinline__ int probe_find(const int32_t* keys, int32_t j, int lg, uint32_t mask) {
-    uint32_t h = fib_hash(j, lg);
+__device__ __forceinline__ int probe_find(const int32_t* keys, int32_t j, int lg, uint32_t mask,
+                                          uint32_t mult = FIB_MULT) {
+    uint32_t h = ((uint32_t)j * mult) >> (32 - lg);
     for (;;) {
         int32_t k = keys[h];
         if (k == j) return (int)h;
@@ -280,6 +281,72 @@ struct WarpProber {
     }
 };
 
+// Collision-free multipliers tried for small plain masks (odd constants).
+__device__ __forceinline__ uint32_t direct_mult(int t) {
+    switch (t) {
+        case 0: return FIB_MULT;
+        case 1: return 0x85EBCA77u;
+        case 2: return 0xC2B2AE3Du;
+        case 3: return 0x27D4EB2Fu;
+        case 4: return 0x165667B1u;
+        case 5: return 0xD3A2646Du;
+        case 6: return 0xFD7046C5u;
+        default: return 0xB55A4F09u;
+    }
+}
+constexpr int DIRECT_TRIES = 8;
+
+// Plain mask whose keys all sit in their home slot (a multiplier without
+// collisions was found for the row): membership is one shared load and one
+// compare, with no probe sequence and nothing to defer.
+template <int KIND, bool NUMERIC>
+struct DirectProber {
+    uint32_t keys_s, cnt_s, val_s;
+    uint32_t mult;
+    int shift;
+    const void* b_val;
+    unsigned evaluated;
+    template <int U>
+    __device__ __forceinline__ void put_batch(const int32_t* j, const long long* a, const long long* s) {
+        uint32_t h[U];
+        int32_t k[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            h[u] = ((uint32_t)j[u] * mult) >> shift;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(k[u]) : "r"(keys_s + (h[u] << 2)));
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool hit = k[u] == j[u] && j[u] >= 0;   // padding lanes carry EMPTY_KEY
+            if (KIND == 0) {
+                // plus-pair: evaluated = sum of the counts, taken at the gather
+                if (NUMERIC)
+                    asm volatile(
+                        "{\n\t.reg .pred ph;\n\t"
+                        "setp.ne.u32 ph, %0, 0;\n\t"
+                        "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"((uint32_t)hit),
+                        "r"(cnt_s + (h[u] << 2))
+                        : "memory");
+                else
+                    asm volatile(
+                        "{\n\t.reg .pred ph;\n\t"
+                        "setp.ne.u32 ph, %0, 0;\n\t"
+                        "@ph st.shared.u32 [%1], 1;\n\t}" ::"r"((uint32_t)hit),
+                        "r"(cnt_s + (h[u] << 2))
+                        : "memory");
+            } else if (hit) {
+                evaluated++;
+                if (NUMERIC) {
+                    const long long prod = a[u] * ((const long long*)b_val)[s[u]];
+                    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(val_s + (h[u] << 3)), "l"(prod) : "memory");
+                }
+                asm volatile("st.shared.u32 [%0], 1;" ::"r"(cnt_s + (h[u] << 2)) : "memory");
+            }
+        }
+    }
+    __device__ __forceinline__ void drain() {}
+};
+
 // Slot locator for the ordered float64 path (single warp).
 template <int MODE>
 struct HashLocatorF64 {
@@ -315,25 +382,67 @@ struct HashLocatorF64 {
 // ---------------------------------------------------------------------------
 template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
-                                         int cap_lg, int gt, int bar_id, int* s_warp,
+                                         int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
                                          BatchSmem bsm, unsigned char* wq,
                                          unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
+    // Plain masks in shared memory keep the table clean between rows (each
+    // row cleans what it touched) and first look for a multiplier that puts
+    // every mask key in its home slot of the full 2^cap_lg_max table.
+    constexpr bool CLEAN = MODE == MODE_PLAIN && SMEM && KIND != 2;
     const int lane = gt & 31;
     const int wg = gt >> 5;
+    const int64_t i = ri.i, as = ri.as, ae = ri.ae, ms = ri.ms, me = ri.me;
+    const int64_t nm = me - ms;
+    bool direct = false;
+    uint32_t mult = FIB_MULT;
+    if (CLEAN && nm * nm <= (1ll << (cap_lg_max + 2))) {
+        const int sh = 32 - cap_lg_max;
+        for (int t = 0; t < DIRECT_TRIES && !direct; t++) {
+            const uint32_t m = direct_mult(t);
+            bool clash = false;
+            for (int64_t q = ms + gt; q < me; q += GT) {
+                const int32_t j = p.m_idx[q];
+                clash |= atomicCAS(&tb.keys[((uint32_t)j * m) >> sh], EMPTY_KEY, j) != EMPTY_KEY;
+            }
+            bool any = __any_sync(FULL, clash);
+            if (GW > 1) {
+                if (lane == 0) s_warp[wg] = any;
+                group_bar(bar_id, GT);
+                any = false;
+#pragma unroll
+                for (int w = 0; w < GW; w++) any |= s_warp[w] != 0;
+                group_bar(bar_id, GT);
+            }
+            if (!any) {
+                direct = true;
+                mult = m;
+            } else {
+                for (int64_t q = ms + gt; q < me; q += GT) {
+                    const int32_t j = p.m_idx[q];
+                    const uint32_t h = ((uint32_t)j * m) >> sh;
+                    if (tb.keys[h] == j) tb.keys[h] = EMPTY_KEY;
+                }
+                group_bar(bar_id, GT);
+            }
+        }
+    }
+    if (direct) cap_lg = cap_lg_max;
+    if (CLEAN) __syncwarp();
     const int cap = 1 << cap_lg;
     const uint32_t cmask = (uint32_t)cap - 1;
-    const int64_t i = ri.i, as = ri.as, ae = ri.ae, ms = ri.ms, me = ri.me;
 
-    // 1. clear the table
-    for (int e = gt; e < cap; e += GT) {
-        tb.keys[e] = EMPTY_KEY;
-        tb.cnt[e] = 0;
-        if (KIND == 1) tb.val[e] = 0ull;
+    // 1. clear the table (CLEAN: already clean)
+    if (!CLEAN) {
+        for (int e = gt; e < cap; e += GT) {
+            tb.keys[e] = EMPTY_KEY;
+            tb.cnt[e] = 0;
+            if (KIND == 1) tb.val[e] = 0ull;
+        }
+        group_bar(bar_id, GT);
     }
-    group_bar(bar_id, GT);
     // 2. mark the mask row (plain: ALLOWED; table complement: NOT-ALLOWED = -1)
-    if (MODE != MODE_CSRCH) {
+    if (MODE != MODE_CSRCH && !direct) {
         for (int64_t t = ms + gt; t < me; t += GT) {
             int32_t j = p.m_idx[t];
             uint32_t h = fib_hash(j, cap_lg);
@@ -351,6 +460,17 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     if (KIND == 2) {
         HashLocatorF64<MODE> loc{tb.keys, tb.cnt, (double*)tb.val, cap_lg, cmask, p.m_idx + ms, me - ms};
         evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+    } else if (CLEAN && direct) {
+        DirectProber<KIND, NUMERIC> pr;
+        pr.keys_s = (uint32_t)__cvta_generic_to_shared(tb.keys);
+        pr.cnt_s = (uint32_t)__cvta_generic_to_shared(tb.cnt);
+        pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(tb.val);
+        pr.mult = mult;
+        pr.shift = 32 - cap_lg;
+        pr.b_val = p.b_val;
+        pr.evaluated = 0;
+        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+        evaluated += pr.evaluated;
     } else {
         WarpProber<KIND, MODE, NUMERIC, SMEM> pr;
         pr.tb = tb;
@@ -384,8 +504,9 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             int h = 0;
             if (t < me) {
                 j = p.m_idx[t];
-                h = probe_find(tb.keys, j, cap_lg, cmask);
+                h = probe_find(tb.keys, j, cap_lg, cmask, mult);
                 set = tb.cnt[h] > 0;
+                if (CLEAN && KIND == 0 && NUMERIC && direct) evaluated += (unsigned)tb.cnt[h];
             }
             int tot;
             int pos = group_prefix<GW>(set, &tot, s_warp, bar_id, gt);
@@ -467,6 +588,24 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     }
     if (gt == 0) o.row_nnz[i] = running;
     group_bar(bar_id, GT);
+    if (CLEAN) {
+        // leave the table clean: the home slots of a direct row, else the row's whole table
+        if (direct) {
+            for (int64_t q = ms + gt; q < me; q += GT) {
+                const uint32_t h = ((uint32_t)p.m_idx[q] * mult) >> (32 - cap_lg);
+                tb.keys[h] = EMPTY_KEY;
+                tb.cnt[h] = 0;
+                if (KIND == 1) tb.val[h] = 0ull;
+            }
+        } else {
+            for (int e = gt; e < cap; e += GT) {
+                tb.keys[e] = EMPTY_KEY;
+                tb.cnt[e] = 0;
+                if (KIND == 1) tb.val[e] = 0ull;
+            }
+        }
+        group_bar(bar_id, GT);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -501,11 +640,19 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
                         (size_t)groups * BATCH_BYTES + (size_t)(threadIdx.x >> 5) * queue_bytes<KIND>();
     Table<KIND> tb;
     tb.bind(base, cap_max);
+    if (MODE == MODE_PLAIN && SMEM && KIND != 2) {   // hash_row keeps it clean from here on
+        for (int e = gt; e < cap_max; e += GT) {
+            tb.keys[e] = EMPTY_KEY;
+            tb.cnt[e] = 0;
+            if (KIND == 1) tb.val[e] = 0ull;
+        }
+        group_bar(bar_id, GT);
+    }
     unsigned long long evaluated = 0;
     RowFetcher<GW> rf;
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
-        hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg[ri.i], gt, bar_id,
+        hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg[ri.i], cap_lg_max, gt, bar_id,
                                                 s_warp + g * GW, bsm, wq, evaluated);
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);
