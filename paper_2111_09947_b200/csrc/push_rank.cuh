@@ -368,7 +368,7 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
 // in dynamic shared memory, otherwise in one global slab per group (tier 3).
 template <int GW, bool SMEM, int KIND, bool MSA, bool NUMERIC>
 #ifndef MM_RANK_MINB
-#define MM_RANK_MINB 1
+#define MM_RANK_MINB 5   // <= 51 registers: 5 blocks of 256 threads per SM (measured best on cfg2)
 #endif
 __global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256), GW <= 8 ? MM_RANK_MINB : 1)
 k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gslab) {
