@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(OUT_DIR, "libmaskmul_b200.so")
 SOURCES = ["maskmul_abi.cu"]
-HEADERS = ["common.cuh", "analyze.cuh", "product_loop.cuh", "push_hash.cuh", "push_rank.cuh", "push_heap.cuh", "push_single.cuh", "push_msa_sparse.cuh",
+HEADERS = ["common.cuh", "analyze.cuh", "product_loop.cuh", "push_hash.cuh", "push_rank.cuh", "push_heap.cuh", "push_single.cuh", "push_msa_sparse.cuh", "push_dense.cuh",
            "pull_inner.cuh", "scan_compact.cuh"]
 
 NVCC_FLAGS = [

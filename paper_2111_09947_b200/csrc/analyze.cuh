@@ -31,9 +31,11 @@ enum Bin : int {
     BIN_HEAP0 = 31,   // + tier
     BIN_SINGLE = 35,  // one A entry: filtered, scaled copy of B_k (auto)
     BIN_MSAS0 = 36,   // + tier (0..2): MSA with a sparse two-level window bitmap
-    NBINS = 39
+    BIN_MSAD0 = 39,   // + tier (0..2): MSA with a dense per-column window (push_dense.cuh)
+    NBINS = 42
 };
 __host__ __device__ constexpr bool is_msas_bin(int b) { return b >= BIN_MSAS0 && b < BIN_MSAS0 + 3; }
+__host__ __device__ constexpr bool is_msad_bin(int b) { return b >= BIN_MSAD0 && b < BIN_MSAD0 + 3; }
 __host__ __device__ constexpr bool is_msa_bin(int b) { return b >= BIN_MSA0 && b < BIN_MSA0 + 4; }
 __host__ __device__ constexpr bool is_mca_bin(int b) { return b >= BIN_MCA0 && b < BIN_MCA0 + 4; }
 __host__ __device__ constexpr bool is_heap_bin(int b) { return b >= BIN_HEAP0 && b < BIN_HEAP0 + 4; }
@@ -102,6 +104,10 @@ __host__ __device__ constexpr int64_t msas_blocks(int64_t words, int64_t nm) {
 __host__ __device__ constexpr int64_t msas_bytes(int64_t words, int64_t nm, int kind) {
     return 2 * msas_dir(words) + 192 * msas_blocks(words, nm) + (kind == 0 ? 4 : 12) * nm;
 }
+// dense window: a state per column of the window plus a guard column
+__host__ __device__ constexpr int64_t msad_bytes(int64_t words, int kind) {
+    return (kind == 0 ? 4 : 12) * (32 * words + 1);
+}
 __host__ __device__ constexpr int64_t mca_bytes(int64_t nm, int kind) {
     return (kind == 0 ? 8 : 16) * nm;
 }
@@ -153,6 +159,8 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         *aux_out = msas_dir(words);                   // per-bin maximum directory length
         return BIN_MSAS0 + tr;
     }
+    // the dense window when it fits: one load and one compare per product
+    if (!ap.comp && fam == FAM_MSA && msad_bytes(words, kind) <= ap.rank_budget[tr]) return BIN_MSAD0 + tr;
     if (!ap.comp && (fam == FAM_MSA || fam == FAM_MCA)) {
         const int64_t bytes = fam == FAM_MSA ? msa_bytes(words, nm, kind) : mca_bytes(nm, kind);
         const int tier = bytes <= ap.rank_budget[tr] ? tr : 3;

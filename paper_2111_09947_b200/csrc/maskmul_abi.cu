@@ -25,6 +25,7 @@
 #include "push_heap.cuh"
 #include "push_single.cuh"
 #include "push_msa_sparse.cuh"
+#include "push_dense.cuh"
 #include "scan_compact.cuh"
 
 using namespace mm;
@@ -236,7 +237,10 @@ template <int KIND, bool MSA, bool NUM>
 RankKernel pick_rank_unordered(int tier, int* gw) {
     switch (tier) {
         case 0: *gw = 1; return k_push_rank<1, true, KIND, MSA, NUM>;
-        case 1: *gw = 4; return k_push_rank<4, true, KIND, MSA, NUM>;
+#ifndef MM_RANK_T1_GW
+#define MM_RANK_T1_GW 4
+#endif
+        case 1: *gw = MM_RANK_T1_GW; return k_push_rank<MM_RANK_T1_GW, true, KIND, MSA, NUM>;
 #ifndef MM_RANK_T2_GW
 #define MM_RANK_T2_GW 8
 #endif
@@ -405,6 +409,38 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             }
             ++g_launches;
             kern<<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max, h->plan.n_inspect, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
+        if (is_msad_bin(b)) {
+            const int tier = b - BIN_MSAD0;
+            const int kind = numeric ? h->kind : 0;
+            void (*kern)(Prob, Out, Work, int) = nullptr;
+            const int gw = kind == 2 ? 1 : (tier == 0 ? 1 : (tier == 1 ? MM_RANK_T1_GW : MM_RANK_T2_GW));
+            if (kind == 2) {
+                kern = k_push_dense<1, 2, true>;
+            } else if (!numeric || kind == 0) {
+                if (gw == 1) kern = numeric ? k_push_dense<1, 0, true> : k_push_dense<1, 0, false>;
+                else if (gw == 4) kern = numeric ? k_push_dense<4, 0, true> : k_push_dense<4, 0, false>;
+                else kern = numeric ? k_push_dense<8, 0, true> : k_push_dense<8, 0, false>;
+            } else {
+                kern = gw == 1 ? k_push_dense<1, 1, true> : (gw == 4 ? k_push_dense<4, 1, true> : k_push_dense<8, 1, true>);
+            }
+            const int groups = 256 / (32 * gw);
+            const int words_max = std::max(h->sum.bin_words[b], 1);
+            const size_t rb = (dense_region_bytes(kind, words_max) + 15) & ~(size_t)15;
+            const size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            const size_t smem = groups * (rb + batch);
+            if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "dense MSA window exceeds shared memory");
+            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            const int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
+            if (debug_launches())
+                fprintf(stderr, "[mm] dense-msa bin %d rows %d gw %d words %d smem %zu grid %d occ %d\n", b, cnt, gw,
+                        words_max, smem, grid, occ);
+            ++g_launches;
+            kern<<<grid, 256, smem, st>>>(h->prob, out, wk, words_max);
             CU(cudaGetLastError());
             continue;
         }

@@ -36,7 +36,7 @@ for tune in tunings or [None]:
             if rep:
                 best_n, best_t = min(best_n, ms[2]), min(best_t, ms[5])
         tri = int(reduce_sum(c.values).item())
-        nb = 39
+        nb = 42
         rows = (C.c_int64 * nb)()
         fl = (C.c_int64 * nb)()
         lib.mm_profile_bins(h, rows, fl, nb)
