@@ -323,7 +323,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             int cap_lg = std::max(h->sum.bin_cap_lg[b], 5);
             size_t ebytes = kind == 0 ? 8 : 16;
             size_t table = ((size_t)1 << cap_lg) * ebytes;
-            size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            size_t batch = batch_bytes_rt(gw, kind);
             size_t queue = kind == 2 ? 0 : (size_t)64 * (kind == 1 ? 24 : 8);
             size_t smem = (smem_table ? groups * table : 0) + groups * batch + (threads / 32) * queue;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "hash tier table exceeds shared memory");
@@ -358,7 +358,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             const int nm_max = std::max(h->sum.bin_nmmax[b], 1);
             size_t rb = rank_region_bytes_rt(kind, msa, words_max, nm_max);
             rb = (rb + 15) & ~(size_t)15;
-            const size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            const size_t batch = batch_bytes_rt(gw, kind);
             const size_t smem = (smem_region ? groups * rb : 0) + groups * batch;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "rank tier region exceeds shared memory");
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -429,7 +429,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             const int groups = 256 / (32 * gw);
             const int words_max = std::max(h->sum.bin_words[b], 1);
             const size_t rb = (dense_region_bytes(kind, words_max) + 15) & ~(size_t)15;
-            const size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            const size_t batch = batch_bytes_rt(gw, kind);
             const size_t smem = groups * (rb + batch);
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "dense MSA window exceeds shared memory");
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -465,7 +465,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             size_t rb = (size_t)(kind == 0 ? 0 : 8) * nm_max + 4 * (size_t)nm_max + 2 * (size_t)((d_max + 1) & ~1) +
                         192 * (size_t)blk_max;
             rb = (rb + 15) & ~(size_t)15;
-            const size_t batch = kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+            const size_t batch = batch_bytes_rt(gw, kind);
             const size_t smem = groups * (rb + batch);
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "sparse MSA region exceeds shared memory");
             CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -123,9 +123,12 @@ struct RowFetcher {
 // Shared-memory staging of one batch of A entries: base of the B row (made
 // relative to the batch's product index), A value (int64 plus-times), and
 // the inclusive product end.  Bytes per group.
+__host__ __device__ constexpr size_t batch_bytes_rt(int gw, int kind) {
+    return kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+}
 template <int GW, int KIND>
 __host__ __device__ constexpr size_t batch_bytes() {
-    return KIND == 2 ? 0 : (size_t)GW * 32 * ((KIND == 1 ? 16 : 8) + 4);
+    return batch_bytes_rt(GW, KIND);
 }
 
 struct BatchSmem {
@@ -133,6 +136,16 @@ struct BatchSmem {
     long long* base;
     long long* av;
 };
+
+template <int GW, int KIND>
+__device__ __forceinline__ BatchSmem bind_batch(unsigned char* bbase) {
+    constexpr int GT = GW * 32;
+    BatchSmem bsm;
+    bsm.base = (long long*)bbase;
+    bsm.av = bsm.base + GT;
+    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    return bsm;
+}
 
 // Order-free accumulation (plus-pair counts, int64 sums) over the row's
 // flattened product space, batch by batch (NB = GT entries of A_i):
@@ -159,7 +172,6 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
     constexpr int CH = 32 * U;
     constexpr int NB = GT;
     const int lane32 = gt & 31;
-    const int wg = gt >> 5;
     for (int64_t tb0 = as; tb0 < ae; tb0 += NB) {
         const int64_t t = tb0 + gt;
         long long base = 0, av = 0;
@@ -179,6 +191,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
             bsm.base[gt] = base - (incl - len);
             if (KIND == 1) bsm.av[gt] = av;
             group_bar(bar_id, GT);
+            const int wg = gt >> 5;
             q_lo = (int)(((long long)tot * wg) / GW);
             q_hi = (int)(((long long)tot * (wg + 1)) / GW);
             int lo = 0, hi = NB - 1;

@@ -197,10 +197,7 @@ k_push_dense(Prob p, Out o, Work wk, int words_max) {
     unsigned long long* val = KIND == 0 ? nullptr : (unsigned long long*)region;
     int32_t* cnt = (int32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)ncol));
     unsigned char* bbase = smem + (size_t)groups * rbytes + (size_t)g * batch_bytes<GW, KIND>();
-    BatchSmem bsm;
-    bsm.base = (long long*)bbase;
-    bsm.av = bsm.base + GT;
-    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    BatchSmem bsm = bind_batch<GW, KIND>(bbase);
     for (int c = gt; c < ncol; c += GT) cnt[c] = DENIED;
     group_bar(bar_id, GT);
     unsigned long long evaluated = 0;

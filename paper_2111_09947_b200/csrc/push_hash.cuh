@@ -635,10 +635,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
                                              HashEntry<KIND>::bytes;
     unsigned char* bbase = smem + (SMEM ? (size_t)groups * cap_max * HashEntry<KIND>::bytes : 0) +
                            (size_t)g * BATCH_BYTES;
-    BatchSmem bsm;
-    bsm.base = (long long*)bbase;
-    bsm.av = bsm.base + GT;
-    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    BatchSmem bsm = bind_batch<GW, KIND>(bbase);
     unsigned char* wq = smem + (SMEM ? (size_t)groups * cap_max * HashEntry<KIND>::bytes : 0) +
                         (size_t)groups * BATCH_BYTES + (size_t)(threadIdx.x >> 5) * queue_bytes<KIND>();
     Table<KIND> tb;

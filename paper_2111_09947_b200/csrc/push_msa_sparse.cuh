@@ -266,10 +266,7 @@ __global__ void __launch_bounds__(256) k_push_msas(Prob p, Out o, Work wk, int d
     const size_t rbytes = (sparse_region_bytes<KIND>(d_max, blk_max, nm_max) + 15) & ~(size_t)15;
     unsigned char* region = smem + (size_t)g * rbytes;
     unsigned char* bbase = smem + (size_t)groups * rbytes + (size_t)g * batch_bytes<GW, KIND>();
-    BatchSmem bsm;
-    bsm.base = (long long*)bbase;
-    bsm.av = bsm.base + GT;
-    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    BatchSmem bsm = bind_batch<GW, KIND>(bbase);
     {
         uint16_t* dir = (uint16_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
         uint32_t* words = (uint32_t*)(dir + ((d_max + 1) & ~1));

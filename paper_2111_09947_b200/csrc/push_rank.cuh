@@ -383,10 +383,7 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     const size_t rbytes = (rank_region_bytes<KIND>(MSA, SMEM, words_max, nm_max) + 15) & ~(size_t)15;
     unsigned char* region = SMEM ? smem + (size_t)g * rbytes : gslab + ((size_t)blockIdx.x * groups + g) * rbytes;
     unsigned char* bbase = smem + (SMEM ? (size_t)groups * rbytes : 0) + (size_t)g * batch_bytes<GW, KIND>();
-    BatchSmem bsm;
-    bsm.base = (long long*)bbase;
-    bsm.av = bsm.base + GT;
-    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    BatchSmem bsm = bind_batch<GW, KIND>(bbase);
     unsigned long long evaluated = 0;
     if (MSA) {
         uint32_t* bits = (uint32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
