@@ -147,6 +147,22 @@ __device__ __forceinline__ BatchSmem bind_batch(unsigned char* bbase) {
     return bsm;
 }
 
+// The last, partial chunk of a long B segment: V predicated loads per lane.
+template <int V, class PR>
+__device__ __forceinline__ void tail_chunk(const Prob& p, PR& pr, const int32_t* bp, int c, int n0, long long a0,
+                                           long long b0, int lane32) {
+    int32_t jj[V];
+    long long aa[V], ss[V];
+#pragma unroll
+    for (int u = 0; u < V; u++) {
+        const int o = c + 32 * u + lane32;
+        jj[u] = o < n0 ? __ldg(bp + o) : EMPTY_KEY;
+        aa[u] = a0;
+        ss[u] = b0 + o;
+    }
+    pr.template put_batch<V>(jj, aa, ss);
+}
+
 // Order-free accumulation (plus-pair counts, int64 sums) over the row's
 // flattened product space, batch by batch (NB = GT entries of A_i):
 //   1. thread gt loads A entry tb0+gt (base of its B row, length); a
@@ -245,17 +261,12 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                     }
                     pr.template put_batch<U>(jj, aa, ss);
                 }
-                if (c < n0) {
-                    int32_t jj[U];
-                    long long aa[U], ss[U];
-#pragma unroll
-                    for (int u = 0; u < U; u++) {
-                        const int o = c + 32 * u + lane32;
-                        jj[u] = o < n0 ? __ldg(bp + o) : EMPTY_KEY;
-                        aa[u] = a0;
-                        ss[u] = b0 + o;
-                    }
-                    pr.template put_batch<U>(jj, aa, ss);
+                if (n0 - c > 32 * U / 2) {        // tail: as many loads as it needs
+                    tail_chunk<U>(p, pr, bp, c, n0, a0, b0, lane32);
+                } else if (n0 - c > 32) {
+                    tail_chunk<U / 2>(p, pr, bp, c, n0, a0, b0, lane32);
+                } else if (c < n0) {
+                    tail_chunk<1>(p, pr, bp, c, n0, a0, b0, lane32);
                 }
             }
             const int slen = plen < 32 ? plen : 0;
