@@ -133,13 +133,15 @@ int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void
 int mm_profile_enable(mm_handle_t* h, int on);
 int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
 /* Kernel-tier tuning of this handle (0 keeps a value): params[0] = max
- * products of a row in the 1-warp tier (default 4096), params[1] = max in the
+ * products of a row in the 1-warp tier (default 8192), params[1] = max in the
  * 4-warp tier (65536), params[2] = log2 table-size class boundary (9),
  * params[3] = preferred table size as keys << params[3] (2, i.e. load 1/4),
  * params[4..6] = shared bytes per row allowed for the MSA / MCA rank-slot
  * accumulators in the 1-, 4- and 16-warp tiers (6144, 24576, 49152),
  * params[7] = AUTO: 1-warp rows whose MSA window does not fit use MCA when
- * their mask row has at most this many entries (0). */
+ * their mask row has at most this many entries (0; negative keeps),
+ * params[8] = log2 of the smallest plain shared-memory hash table, which
+ * leaves room for a collision-free (direct-mapped) table (9; 0 = bin size). */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

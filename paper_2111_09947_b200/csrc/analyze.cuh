@@ -88,7 +88,7 @@ struct AnalyzeParams {
     int has_bt;      // B^T (CSC) available
 };
 
-__device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
+__host__ __device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
     return pair ? tier_cap_lg_pair(tier) : tier_cap_lg_val(tier);
 }
 
