@@ -98,7 +98,7 @@ struct mm_handle {
     int capc_lg = CAPC_LG, load_shift = 2;
     int rank_budget[3] = {6144, 24576, 49152};
     int auto_mca_nm = 0;
-    int direct_lg = 9;                 // plain shared hash tables: at least 2^direct_lg slots (0 = bin size)
+    int direct_lg[3] = {9, 10, 12};    // plain shared hash tables per tier: at least 2^direct_lg slots (0 = bin size)
     // ---- concurrent bin launches ----
     static constexpr int NAUX = 3;
     cudaStream_t aux[NAUX] = {};
@@ -323,8 +323,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             int groups = threads / (32 * gw);
             int cap_lg = std::max(h->sum.bin_cap_lg[b], 5);
             // plain masks in shared memory: room for collision-free direct tables
-            if (mode == MODE_PLAIN && smem_table && kind != 2 && h->direct_lg > cap_lg)
-                cap_lg = std::min(h->direct_lg, tier_cap_lg(kind == 0, tier));
+            if (mode == MODE_PLAIN && smem_table && kind != 2 && h->direct_lg[tier] > cap_lg)
+                cap_lg = std::min(h->direct_lg[tier], tier_cap_lg(kind == 0, tier));
             size_t ebytes = kind == 0 ? 8 : 16;
             size_t table = ((size_t)1 << cap_lg) * ebytes;
             size_t batch = batch_bytes_rt(gw, kind);
@@ -839,7 +839,8 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     for (int t = 0; t < 3; t++)
         if (n > 4 + t && params[4 + t] > 0) h->rank_budget[t] = (int)params[4 + t];
     if (n > 7 && params[7] >= 0) h->auto_mca_nm = (int)params[7];
-    if (n > 8 && params[8] >= 0 && params[8] <= 14) h->direct_lg = (int)params[8];
+    for (int t = 0; t < 3; t++)
+        if (n > 8 + t && params[8 + t] >= 0 && params[8 + t] <= 14) h->direct_lg[t] = (int)params[8 + t];
     return MM_OK;
 }
 

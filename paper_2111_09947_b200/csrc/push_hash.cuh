@@ -617,7 +617,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
 #define MM_HASH_MINB 4   // <= 64 registers: 4 blocks of 256 threads per SM (5 spills; measured on cfg2)
 #endif
 template <int GW, bool SMEM, int KIND, int MODE, bool NUMERIC>
-__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256), GW <= 8 ? MM_HASH_MINB : 1)
+__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256), GW <= 8 ? MM_HASH_MINB : (GW == 16 ? 2 : 1))
 k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
             unsigned char* gslab) {
     extern __shared__ __align__(16) unsigned char smem[];

@@ -15,9 +15,12 @@ da = DeviceCsr.from_host(w.a, dtype=dt, with_values=vals)
 db = da if w.b is w.a else DeviceCsr.from_host(w.b, dtype=dt, with_values=vals)
 bt = db.transpose_storage() if algo == "inner" else None
 lib = _lib.load(); h = _handle(0); lib.mm_profile_enable(h, 1)
+if os.environ.get("TUNE"):
+    prm = [int(x) for x in os.environ["TUNE"].split(":")]
+    lib.mm_set_tuning(h, (C.c_int64 * len(prm))(*prm), len(prm))
 plan = MultiplyPlan(algorithm=algo, semiring=w.semiring, complemented=w.complemented)
 for _ in range(reps):
     c, st = multiply_device(dm, da, db, plan, b_csc=bt)
 ms = (C.c_float * 6)(); lib.mm_profile_read(h, ms, 6, None)
 rows = (C.c_int64 * 42)(); fl = (C.c_int64 * 42)(); lib.mm_profile_bins(h, rows, fl, 42)
-print(name, algo, [round(x, 3) for x in ms], {b: (rows[b], fl[b]) for b in range(42) if rows[b]})
+print(name, algo, os.environ.get("TUNE", ""), [round(x, 3) for x in ms], {b: (rows[b], fl[b]) for b in range(42) if rows[b]})
