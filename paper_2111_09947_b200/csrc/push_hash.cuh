@@ -296,28 +296,69 @@ __device__ __forceinline__ uint32_t direct_mult(int t) {
 }
 constexpr int DIRECT_TRIES = 8;
 
-// Plain mask whose keys all sit in their home slot (a multiplier without
-// collisions was found for the row): membership is one shared load and one
-// compare, with no probe sequence and nothing to defer.
-template <int KIND, bool NUMERIC>
+constexpr int CUCKOO_TRIES = 4;
+constexpr int CUCKOO_MAXIT = 64;
+
+// Where the mask keys of a plain row sit.  hm = 0: linear probing from the
+// Fibonacci hash; hm = 1 (direct): every key in its home slot
+// (j * m1) >> (32 - lg); hm = 2 (two-choice cuckoo): every key in one of its
+// two candidate slots, (j * m1) >> (33 - lg) in the lower half of the table
+// or half + (j * m2) >> (33 - lg) in the upper half.
+struct Placement {
+    int hm;
+    int lg;
+    uint32_t m1, m2;
+    __device__ __forceinline__ uint32_t h1(int32_t j) const {
+        return hm == 2 ? ((uint32_t)j * m1) >> (33 - lg) : ((uint32_t)j * m1) >> (32 - lg);
+    }
+    __device__ __forceinline__ uint32_t h2(int32_t j) const {
+        return (1u << (lg - 1)) + (((uint32_t)j * m2) >> (33 - lg));
+    }
+    // slot of a key known to be in the table
+    __device__ __forceinline__ int slot(const int32_t* keys, int32_t j) const {
+        if (hm == 1) return (int)h1(j);
+        if (hm == 2) {
+            const uint32_t a = h1(j);
+            return keys[a] == j ? (int)a : (int)h2(j);
+        }
+        return probe_find(keys, j, lg, (1u << lg) - 1u, m1);
+    }
+};
+
+// Plain mask with every key at a fixed candidate slot (direct: one, cuckoo:
+// two): membership is one or two independent shared loads and compares, with
+// no probe sequence and nothing to defer.
+template <int KIND, bool NUMERIC, int WAYS>
 struct DirectProber {
     uint32_t keys_s, cnt_s, val_s;
-    uint32_t mult;
-    int shift;
+    uint32_t mult, mult2;
+    int shift;            // 32 - lg (direct) or 33 - lg (cuckoo, per half)
+    uint32_t half;        // cuckoo: first slot of the upper half
     const void* b_val;
     unsigned evaluated;
     template <int U>
     __device__ __forceinline__ void put_batch(const int32_t* j, const long long* a, const long long* s) {
         uint32_t h[U];
         int32_t k[U];
+        uint32_t hb[U];
+        int32_t kb[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             h[u] = ((uint32_t)j[u] * mult) >> shift;
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(k[u]) : "r"(keys_s + (h[u] << 2)));
+            if (WAYS == 2) {
+                hb[u] = half + (((uint32_t)j[u] * mult2) >> shift);
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(kb[u]) : "r"(keys_s + (hb[u] << 2)));
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const bool hit = k[u] == j[u] && j[u] >= 0;   // padding lanes carry EMPTY_KEY
+            bool hit = k[u] == j[u];
+            if (WAYS == 2) {
+                if (!hit) h[u] = hb[u];
+                hit |= kb[u] == j[u];
+            }
+            hit &= j[u] >= 0;   // padding lanes carry EMPTY_KEY
             if (KIND == 0) {
                 // plus-pair: evaluated = sum of the counts, taken at the gather
                 if (NUMERIC)
@@ -394,29 +435,32 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     const int wg = gt >> 5;
     const int64_t i = ri.i, as = ri.as, ae = ri.ae, ms = ri.ms, me = ri.me;
     const int64_t nm = me - ms;
-    bool direct = false;
-    uint32_t mult = FIB_MULT;
+    Placement pl{0, cap_lg, FIB_MULT, 0u};
+    // group-wide OR of a per-thread flag
+    auto group_any = [&](bool v) {
+        bool any = __any_sync(FULL, v);
+        if (GW > 1) {
+            if (lane == 0) s_warp[wg] = any;
+            group_bar(bar_id, GT);
+            any = false;
+#pragma unroll
+            for (int w = 0; w < GW; w++) any |= s_warp[w] != 0;
+            group_bar(bar_id, GT);
+        }
+        return any;
+    };
     if (CLEAN && nm * nm <= (1ll << (cap_lg_max + 2))) {
+        // direct: a multiplier without collisions over the whole 2^cap_lg_max table
         const int sh = 32 - cap_lg_max;
-        for (int t = 0; t < DIRECT_TRIES && !direct; t++) {
+        for (int t = 0; t < DIRECT_TRIES && pl.hm == 0; t++) {
             const uint32_t m = direct_mult(t);
             bool clash = false;
             for (int64_t q = ms + gt; q < me; q += GT) {
                 const int32_t j = p.m_idx[q];
                 clash |= atomicCAS(&tb.keys[((uint32_t)j * m) >> sh], EMPTY_KEY, j) != EMPTY_KEY;
             }
-            bool any = __any_sync(FULL, clash);
-            if (GW > 1) {
-                if (lane == 0) s_warp[wg] = any;
-                group_bar(bar_id, GT);
-                any = false;
-#pragma unroll
-                for (int w = 0; w < GW; w++) any |= s_warp[w] != 0;
-                group_bar(bar_id, GT);
-            }
-            if (!any) {
-                direct = true;
-                mult = m;
+            if (!group_any(clash)) {
+                pl = Placement{1, cap_lg_max, m, 0u};
             } else {
                 for (int64_t q = ms + gt; q < me; q += GT) {
                     const int32_t j = p.m_idx[q];
@@ -427,11 +471,38 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             }
         }
     }
-    if (direct) cap_lg = cap_lg_max;
+    if (CLEAN && pl.hm == 0 && cap_lg >= 4) {
+        // two-choice cuckoo in the row's table (load <= 1/2 by construction):
+        // atomicExch insertion, each displaced key moved to its other slot
+        const uint32_t half = 1u << (cap_lg - 1);
+        for (int t = 0; t < CUCKOO_TRIES && pl.hm == 0; t++) {
+            const Placement c{2, cap_lg, direct_mult(2 * t), direct_mult(2 * t + 1)};
+            bool lost = false;
+            for (int64_t q = ms + gt; q < me; q += GT) {
+                int32_t cur = p.m_idx[q];
+                uint32_t h = c.h1(cur);
+                int it = 0;
+                for (; it < CUCKOO_MAXIT; it++) {
+                    const int32_t old = atomicExch(&tb.keys[h], cur);
+                    if (old == EMPTY_KEY) break;
+                    cur = old;
+                    h = h < half ? c.h2(cur) : c.h1(cur);
+                }
+                lost |= it == CUCKOO_MAXIT;
+            }
+            if (!group_any(lost)) {
+                pl = c;
+            } else {
+                for (int e = gt; e < (1 << cap_lg); e += GT) tb.keys[e] = EMPTY_KEY;
+                group_bar(bar_id, GT);
+            }
+        }
+    }
+    if (pl.hm == 1) cap_lg = cap_lg_max;
     if (CLEAN) __syncwarp();
     const int cap = 1 << cap_lg;
     const uint32_t cmask = (uint32_t)cap - 1;
-
+    pl.lg = cap_lg;
     // 1. clear the table (CLEAN: already clean)
     if (!CLEAN) {
         for (int e = gt; e < cap; e += GT) {
@@ -442,7 +513,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         group_bar(bar_id, GT);
     }
     // 2. mark the mask row (plain: ALLOWED; table complement: NOT-ALLOWED = -1)
-    if (MODE != MODE_CSRCH && !direct) {
+    if (MODE != MODE_CSRCH && pl.hm == 0) {
         for (int64_t t = ms + gt; t < me; t += GT) {
             int32_t j = p.m_idx[t];
             uint32_t h = fib_hash(j, cap_lg);
@@ -460,13 +531,28 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     if (KIND == 2) {
         HashLocatorF64<MODE> loc{tb.keys, tb.cnt, (double*)tb.val, cap_lg, cmask, p.m_idx + ms, me - ms};
         evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
-    } else if (CLEAN && direct) {
-        DirectProber<KIND, NUMERIC> pr;
+    } else if (CLEAN && pl.hm == 1) {
+        DirectProber<KIND, NUMERIC, 1> pr;
         pr.keys_s = (uint32_t)__cvta_generic_to_shared(tb.keys);
         pr.cnt_s = (uint32_t)__cvta_generic_to_shared(tb.cnt);
         pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(tb.val);
-        pr.mult = mult;
+        pr.mult = pl.m1;
+        pr.mult2 = 0u;
         pr.shift = 32 - cap_lg;
+        pr.half = 0u;
+        pr.b_val = p.b_val;
+        pr.evaluated = 0;
+        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+        evaluated += pr.evaluated;
+    } else if (CLEAN && pl.hm == 2) {
+        DirectProber<KIND, NUMERIC, 2> pr;
+        pr.keys_s = (uint32_t)__cvta_generic_to_shared(tb.keys);
+        pr.cnt_s = (uint32_t)__cvta_generic_to_shared(tb.cnt);
+        pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(tb.val);
+        pr.mult = pl.m1;
+        pr.mult2 = pl.m2;
+        pr.shift = 33 - cap_lg;
+        pr.half = 1u << (cap_lg - 1);
         pr.b_val = p.b_val;
         pr.evaluated = 0;
         flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
@@ -504,9 +590,9 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             int h = 0;
             if (t < me) {
                 j = p.m_idx[t];
-                h = probe_find(tb.keys, j, cap_lg, cmask, mult);
+                h = CLEAN ? pl.slot(tb.keys, j) : probe_find(tb.keys, j, cap_lg, cmask);
                 set = tb.cnt[h] > 0;
-                if (CLEAN && KIND == 0 && NUMERIC && direct) evaluated += (unsigned)tb.cnt[h];
+                if (CLEAN && KIND == 0 && NUMERIC && pl.hm != 0) evaluated += (unsigned)tb.cnt[h];
             }
             int tot;
             int pos = group_prefix<GW>(set, &tot, s_warp, bar_id, gt);
@@ -589,10 +675,10 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     if (gt == 0) o.row_nnz[i] = running;
     group_bar(bar_id, GT);
     if (CLEAN) {
-        // leave the table clean: the home slots of a direct row, else the row's whole table
-        if (direct) {
+        // leave the table clean: the key slots of a direct / cuckoo row, else the row's whole table
+        if (pl.hm != 0) {
             for (int64_t q = ms + gt; q < me; q += GT) {
-                const uint32_t h = ((uint32_t)p.m_idx[q] * mult) >> (32 - cap_lg);
+                const int h = pl.slot(tb.keys, p.m_idx[q]);
                 tb.keys[h] = EMPTY_KEY;
                 tb.cnt[h] = 0;
                 if (KIND == 1) tb.val[h] = 0ull;
