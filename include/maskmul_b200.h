@@ -142,7 +142,8 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
  * their mask row has at most this many entries (0; negative keeps),
  * params[8..10] = log2 of the smallest plain shared-memory hash table in the
  * 1-, 4- and 16-warp tiers, which leaves room for a collision-free
- * (direct-mapped) table (9, 10, 12; 0 = bin size; negative keeps). */
+ * (direct-mapped) table (9, 10, 12; 0 = bin size; negative keeps),
+ * params[11] = params[3] for plain rows of the 16-warp tier (1). */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

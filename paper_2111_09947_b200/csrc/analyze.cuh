@@ -78,6 +78,7 @@ struct AnalyzeParams {
     long long tier_flops1;   // ... 4-warp tier; above: 16-warp tier
     int capc_lg;             // table-size class boundary (log2 slots)
     int load_shift;          // preferred table size = keys << load_shift
+    int load_shift_wide;     // same for plain rows of the 16-warp tier
     int rank_budget[3];      // MSA / MCA shared bytes per group allowed in tiers 0..2
     int auto_mca_nm;         // AUTO: 1-warp rows whose MSA window is too wide use MCA if nm <= this
     int family;      // Family
@@ -187,8 +188,6 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     }
     int need = ceil_log2_i64(2 * keys);
     if (need < 5) need = 5;
-    int want = ceil_log2_i64(keys << ap.load_shift);
-    if (want < 5) want = 5;
     int tier;
     if (ap.ordered) {
         tier = need <= tier_cap_lg_val(0) ? 0 : 3;
@@ -202,6 +201,11 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         const int tfm = mode == MODE_CSRCH ? (flops <= 64 ? 0 : (flops <= 1024 ? 1 : 2)) : tf;
         tier = tc > tfm ? tc : tfm;
     }
+    // wide plain rows (16-warp tier) hold their keys by two-choice cuckoo
+    // placement, which needs only load <= 1/2: smaller tables, more blocks
+    const int ls = tier == 2 && mode == MODE_PLAIN ? ap.load_shift_wide : ap.load_shift;
+    int want = ceil_log2_i64(keys << ls);
+    if (want < 5) want = 5;
     int lim = tier_cap_lg(ap.pair, tier);
     const int used = want < lim ? want : lim;
     *cap_lg_out = used;

@@ -95,7 +95,7 @@ struct mm_handle {
     int bound_flag = 0;
     // ---- tuning (mm_set_tuning) ----
     long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;   // defaults: analyze.cuh
-    int capc_lg = CAPC_LG, load_shift = 2;
+    int capc_lg = CAPC_LG, load_shift = 2, load_shift_wide = 1;
     int rank_budget[3] = {6144, 24576, 49152};
     int auto_mca_nm = 0;
     int direct_lg[3] = {9, 10, 12};    // plain shared hash tables per tier: at least 2^direct_lg slots (0 = bin size)
@@ -567,6 +567,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     ap.tier_flops1 = h->tier_flops1;
     ap.capc_lg = h->capc_lg;
     ap.load_shift = h->load_shift;
+    ap.load_shift_wide = h->load_shift_wide;
     for (int t = 0; t < 3; t++) ap.rank_budget[t] = h->rank_budget[t];
     ap.auto_mca_nm = h->auto_mca_nm;
     ap.comp = comp;
@@ -841,6 +842,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 7 && params[7] >= 0) h->auto_mca_nm = (int)params[7];
     for (int t = 0; t < 3; t++)
         if (n > 8 + t && params[8 + t] >= 0 && params[8 + t] <= 14) h->direct_lg[t] = (int)params[8 + t];
+    if (n > 11 && params[11] > 0 && params[11] <= 4) h->load_shift_wide = (int)params[11];
     return MM_OK;
 }
 
