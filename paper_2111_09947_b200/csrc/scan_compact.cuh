@@ -68,6 +68,29 @@ __global__ void k_set_zero_i64(int64_t* p) { *p = 0; }
 // range.  Work is proportional to nnz(C) whatever the row-length skew.  The
 // one-phase bound assertion (multiply.py:390) is checked row-parallel: a row
 // that overran its slot range raises flag (MM_ERR_INTERNAL at the ABI).
+// Last r in [lo, hi] with ptr[r] <= e (ptr non-decreasing, ptr[lo] <= e),
+// by a 32-ary search: each round the warp probes 32 evenly spaced rows, so a
+// million rows take 4 dependent loads instead of 20.  All lanes call.
+__device__ __forceinline__ int64_t warp_upper_row(const int64_t* ptr, int64_t lo, int64_t hi, int64_t e, int lane) {
+    while (hi - lo >= 32) {
+        const int64_t step = (hi - lo) >> 5;         // probes lo + step .. lo + 32 step <= hi
+        const int64_t probe = lo + (int64_t)(lane + 1) * step;
+        const bool le = __ldg(ptr + probe) <= e;
+        const unsigned bal = __ballot_sync(FULL, le);
+        if (bal == 0) {
+            hi = lo + step - 1;
+        } else {
+            const int top = 31 - __clz(bal);            // probes are monotone: bal is a prefix
+            lo = lo + (int64_t)(top + 1) * step;
+            if (top < 31) hi = lo + step - 1;
+        }
+    }
+    const int64_t probe = lo + lane;
+    const bool le = probe <= hi && __ldg(ptr + probe) <= e;
+    const unsigned bal = __ballot_sync(FULL, le);
+    return lo + (31 - __clz(bal));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* bounds_off,
                                                  const int64_t* row_nnz, const int32_t* tmp_idx,
@@ -82,34 +105,46 @@ __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* b
     const int64_t total = out_ptr[nrows];
     const int64_t warp = gtid >> 5;
     const int64_t nwarps = nthreads >> 5;
-    constexpr int PER = 256;
+    constexpr int PER = 128;
     for (int64_t e0 = warp * PER; e0 < total; e0 += nwarps * PER) {
         const int64_t e1 = e0 + PER < total ? e0 + PER : total;
-        // row span of [e0, e1): last row r with out_ptr[r] <= e
-        int64_t r_lo = 0, r_hi = 0;
-        if (lane < 2) {
-            const int64_t e = lane == 0 ? e0 : e1 - 1;
-            int64_t lo = 0, hi = nrows;   // search over out_ptr[0..nrows]
-            while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) >> 1;
-                if (out_ptr[mid] <= e) lo = mid; else hi = mid - 1;
-            }
-            r_lo = lo;
-        }
-        r_hi = shfl64(r_lo, 1);
-        r_lo = shfl64(r_lo, 0);
-#pragma unroll 4
-        for (int u = 0; u < PER / 32; u++) {
-            const int64_t e = e0 + u * 32 + lane;
-            if (e < e1) {
-                int64_t lo = r_lo, hi = r_hi;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi + 1) >> 1;
-                    if (__ldg(out_ptr + mid) <= e) lo = mid; else hi = mid - 1;
+        // rows holding the tile's first and last entry (last r with out_ptr[r] <= e)
+        const int64_t r_lo = warp_upper_row(out_ptr, 0, nrows, e0, lane);
+        const int64_t r_hi = warp_upper_row(out_ptr, r_lo, nrows, e1 - 1, lane);
+        if (r_hi - r_lo < 32) {
+            // row ends of the span held one per lane; owner by a shuffle search
+            const int64_t r = r_lo + lane;
+            const int64_t end = r <= r_hi ? __ldg(out_ptr + r + 1) : INT64_MAX;
+            const int64_t boff = r <= r_hi ? __ldg(bounds_off + r) - __ldg(out_ptr + r) : 0;
+#pragma unroll
+            for (int u = 0; u < PER / 32; u++) {
+                const int64_t e = e0 + u * 32 + lane;
+                int l = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    const int64_t v = shfl64(end, l + step - 1);
+                    if (v <= e) l += step;
                 }
-                const int64_t src = bounds_off[lo] + (e - out_ptr[lo]);
-                out_idx[e] = tmp_idx[src];
-                out_val[e] = tmp_val[src];
+                const int64_t src = shfl64(boff, l) + e;
+                if (e < e1) {
+                    out_idx[e] = tmp_idx[src];
+                    out_val[e] = tmp_val[src];
+                }
+            }
+        } else {
+#pragma unroll 4
+            for (int u = 0; u < PER / 32; u++) {
+                const int64_t e = e0 + u * 32 + lane;
+                if (e < e1) {
+                    int64_t lo = r_lo, hi = r_hi;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi + 1) >> 1;
+                        if (__ldg(out_ptr + mid) <= e) lo = mid; else hi = mid - 1;
+                    }
+                    const int64_t src = bounds_off[lo] + (e - out_ptr[lo]);
+                    out_idx[e] = tmp_idx[src];
+                    out_val[e] = tmp_val[src];
+                }
             }
         }
     }

@@ -318,3 +318,47 @@ def test_triangle_count_and_k_truss_graph_kernels():
                               np.ones(int(keep.sum()), dtype=np.int64))
         got = k_truss(g, 5, MultiplyPlan(algorithm="hash")).value
         assert np.array_equal(got.row_ptr, cur.row_ptr) and np.array_equal(got.col_idx, cur.col_idx[: cur.nnz])
+
+
+@pytest.mark.parametrize("shape", ["tiny_rows", "skewed", "all_empty_but_one"])
+def test_compact_rows_row_search_edges(shape):
+    """mm_compact_rows against numpy: many 0/1-entry rows (the 32-ary row
+    search with spans of exactly 32 rows), a few huge rows, empty rows."""
+    import ctypes as C
+
+    from paper_2111_09947_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    n = 200_003
+    if shape == "tiny_rows":
+        cnt = rng.integers(0, 2, n)
+    elif shape == "skewed":
+        cnt = rng.integers(0, 3, n)
+        cnt[rng.integers(0, n, 20)] = rng.integers(1000, 50_000, 20)
+    else:
+        cnt = np.zeros(n, np.int64)
+        cnt[n // 2] = 70_000
+    cnt = cnt.astype(np.int64)
+    slack = rng.integers(0, 4, n).astype(np.int64)
+    bounds = np.zeros(n + 1, np.int64)
+    np.cumsum(cnt + slack, out=bounds[1:])
+    out_ptr = np.zeros(n + 1, np.int64)
+    np.cumsum(cnt, out=out_ptr[1:])
+    tmp_idx = rng.integers(0, 1 << 30, int(bounds[-1])).astype(np.int32)
+    tmp_val = rng.integers(-(1 << 40), 1 << 40, int(bounds[-1])).astype(np.int64)
+    keep = np.concatenate([np.arange(bounds[i], bounds[i] + cnt[i]) for i in np.nonzero(cnt)[0]]) \
+        if cnt.sum() else np.zeros(0, np.int64)
+    dev = "cuda"
+    t = {k: torch.from_numpy(v).to(dev) for k, v in
+         dict(bounds=bounds, cnt=cnt, idx=tmp_idx, val=tmp_val, out_ptr=out_ptr).items()}
+    oi = torch.empty(max(int(cnt.sum()), 1), dtype=torch.int32, device=dev)
+    ov = torch.empty(max(int(cnt.sum()), 1), dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    rc = lib.mm_compact_rows(n, t["bounds"].data_ptr(), t["cnt"].data_ptr(), t["idx"].data_ptr(),
+                             t["val"].data_ptr(), t["out_ptr"].data_ptr(), oi.data_ptr(), ov.data_ptr(),
+                             0, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    m = int(cnt.sum())
+    assert np.array_equal(oi[:m].cpu().numpy(), tmp_idx[keep])
+    assert np.array_equal(ov[:m].cpu().numpy(), tmp_val[keep])
