@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
                 if (lane == src) pull_cols = g;
             }
         }
-        int b = -1;
+        int b = -1, cap_lg = 0;
+        int64_t words = 0;
         if (live) {
             const int64_t na = ae - as;
             row_flops[i] = f;
@@ -301,22 +302,35 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
                 bound[i] = bd;
                 my_bound += bd;
             }
-            int cap_lg;
-            int64_t words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
+            words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
             b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg, &words);
             row_bin[i] = (uint8_t)b;
             row_cap_lg[i] = (int8_t)cap_lg;
-            atomicAdd(&s_bflops[b], (unsigned long long)f);
-            if (cap_lg) atomicMax(&s_cap[b], cap_lg);
-            if (b != BIN_EMPTY) {
-                atomicMax(&s_words[b], (int)(words < 0x7fffffff ? words : 0x7fffffff));
-                atomicMax(&s_nmx[b], (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
-            }
             my_flops += f;
         }
-        // warp-aggregated row counts and maxima
-        const unsigned peers = __match_any_sync(FULL, b);
-        if (live && lane == __ffs(peers) - 1) atomicAdd(&s_count[b], __popc(peers));
+        // per-bin sums and maxima, aggregated over the warp's rows of each bin
+        // (one shared atomic per distinct bin instead of one per row)
+        unsigned todo = __ballot_sync(FULL, live);
+        while (todo) {
+            const int leader = __ffs(todo) - 1;
+            const int bl = __shfl_sync(FULL, b, leader);
+            const bool in = live && b == bl;
+            const unsigned peers = __ballot_sync(FULL, in);
+            todo &= ~peers;
+            const long long fs = warp_sum_ll(in ? f : 0);
+            const int capm = __reduce_max_sync(FULL, in ? cap_lg : 0);
+            const int wm = __reduce_max_sync(FULL, in ? (int)(words < 0x7fffffff ? words : 0x7fffffff) : 0);
+            const int nmm = __reduce_max_sync(FULL, in ? (int)(nm < 0x7fffffff ? nm : 0x7fffffff) : 0);
+            if (lane == leader) {
+                atomicAdd(&s_count[bl], __popc(peers));
+                atomicAdd(&s_bflops[bl], (unsigned long long)fs);
+                if (capm) atomicMax(&s_cap[bl], capm);
+                if (bl != BIN_EMPTY) {
+                    atomicMax(&s_words[bl], wm);
+                    atomicMax(&s_nmx[bl], nmm);
+                }
+            }
+        }
         const int na_max = __reduce_max_sync(FULL, live ? (int)min(ae - as, (int64_t)0x7fffffff) : 0);
         const int nm_max = __reduce_max_sync(FULL, live ? (int)min(nm, (int64_t)0x7fffffff) : 0);
         if (lane == 0) {

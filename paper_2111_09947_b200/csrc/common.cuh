@@ -80,6 +80,10 @@ __device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
     return (int64_t)__shfl_sync(FULL, (long long)v, src);
 }
 
+__device__ __forceinline__ long long shfl_up64(long long v, int d) {
+    return __shfl_up_sync(FULL, v, d);
+}
+
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
