@@ -215,7 +215,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
 // One warp per row.  Computes row_flops, 1P complement bounds, bin + table size.
 __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64_t* row_flops,
                                                  int64_t* bound, uint8_t* row_bin, int8_t* row_cap_lg,
-                                                 Summary* s) {
+                                                 Summary* s, int64_t* row_nnz) {
     __shared__ int s_count[NBINS];
     __shared__ int s_cap[NBINS];
     __shared__ unsigned long long s_bflops[NBINS];
@@ -306,6 +306,8 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
             b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg, &words);
             row_bin[i] = (uint8_t)b;
             row_cap_lg[i] = (int8_t)cap_lg;
+            // rows no kernel visits still need a count of 0
+            if (row_nnz && b == BIN_EMPTY) row_nnz[i] = 0;
             my_flops += f;
         }
         // per-bin sums and maxima, aggregated over the warp's rows of each bin
@@ -363,9 +365,21 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
 }
 
 // Scatter row ids into per-bin lists (warp-aggregated atomics).
+// Bin offsets come from the analysis summary (same rule as the host:
+// off[0] = 0, off[b+1] = off[b] + (b == BIN_EMPTY ? 0 : count[b])).
 __global__ void __launch_bounds__(256) k_bin_scatter(int64_t nrows, const uint8_t* row_bin,
-                                                     const int32_t* bin_off, int32_t* bin_cursor,
+                                                     const Summary* s, int32_t* bin_cursor,
                                                      int32_t* rows_out) {
+    __shared__ int32_t bin_off[NBINS + 1];
+    if (threadIdx.x == 0) {
+        int run = 0;
+        bin_off[0] = 0;
+        for (int b = 0; b < NBINS; b++) {
+            run += b == BIN_EMPTY ? 0 : s->bin_count[b];
+            bin_off[b + 1] = run;
+        }
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nrows;
          base += (int64_t)gridDim.x * blockDim.x) {

@@ -81,8 +81,8 @@ struct mm_handle {
     uint8_t* row_bin = nullptr;
     int8_t* row_cap_lg = nullptr;
     int32_t* rows_list = nullptr;
-    int32_t* cursors = nullptr;        // 2 * NBINS fetch counters
-    int32_t* d_bin_off = nullptr;
+    int32_t* cursors = nullptr;        // 3 * NBINS fetch counters (scatter, symbolic, numeric)
+    int64_t* scan_scratch = nullptr;
     int64_t* row_nnz = nullptr;
     int64_t* row_nnz2 = nullptr;
     int64_t* c_row_ptr = nullptr;
@@ -128,39 +128,57 @@ void release(mm_handle* h) {
 }
 
 // ---- scan ----
-int scan_impl(const int64_t* in, int64_t n, int64_t* out_incl, cudaStream_t st,
-              std::vector<void*>& tmp) {
-    // out_incl[0..n) = inclusive scan of in
-    if (n <= 0) return MM_OK;
-    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-    int64_t* partials = nullptr;
-    CU(cudaMallocAsync((void**)&partials, (nb + 1) * sizeof(int64_t), st));
-    tmp.push_back(partials);
+// Scratch (int64 elements) a scan of n items needs: partials and their
+// exclusive scan per level.
+int64_t scan_scratch_elems(int64_t n) {
+    int64_t total = 0;
+    while (n > 0) {
+        const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+        total += 2 * (nb + 1);
+        if (nb <= 1) break;
+        n = nb;
+    }
+    return total;
+}
+
+// out_incl[0..n) = inclusive scan of in (n >= 1); scratch holds
+// scan_scratch_elems(n) elements.  zero_prev: also out_incl[-1] = 0.
+// bounds_off/flag: one-phase bound check of `in`; total: grand total.
+int scan_impl(const int64_t* in, int64_t n, int64_t* out_incl, cudaStream_t st, int64_t* scratch,
+              int zero_prev, const int64_t* bounds_off, int* flag, long long* total) {
+    const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    int64_t* partials = scratch;
+    int64_t* pscan = scratch + (nb + 1);
     ++g_launches;
-    k_scan_tile<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, out_incl, partials);
+    k_scan_tile<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, out_incl, partials, zero_prev, bounds_off, flag,
+                                                       total);
     if (nb > 1) {
-        int64_t* pscan = nullptr;
-        CU(cudaMallocAsync((void**)&pscan, (nb + 1) * sizeof(int64_t), st));
-        tmp.push_back(pscan);
         // exclusive offsets per tile: pscan[0] = 0, pscan[1..nb] = incl(partials)
-        ++g_launches;
-        k_set_zero_i64<<<1, 1, 0, st>>>(pscan);
-        int rc = scan_impl(partials, nb, pscan + 1, st, tmp);
+        int rc = scan_impl(partials, nb, pscan + 1, st, scratch + 2 * (nb + 1), 1, nullptr, nullptr, nullptr);
         if (rc) return rc;
         ++g_launches;
-        k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out_incl, n, pscan);
+        k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out_incl, n, pscan, total);
     }
     CU(cudaGetLastError());
     return MM_OK;
 }
 
-int exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, cudaStream_t st) {
-    std::vector<void*> tmp;
-    ++g_launches;
-    k_set_zero_i64<<<1, 1, 0, st>>>(out);
-    int rc = scan_impl(counts, n, out + 1, st, tmp);
-    for (void* q : tmp) cudaFreeAsync(q, st);
-    CU(cudaGetLastError());
+// out[0] = 0, out[1..n] = inclusive scan of counts.  scratch: caller-owned
+// (scan_scratch_elems(n) elements) or nullptr (allocated from the pool).
+int exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, cudaStream_t st, int64_t* scratch = nullptr,
+                   const int64_t* bounds_off = nullptr, int* flag = nullptr, long long* total = nullptr) {
+    if (n <= 0) {
+        CU(cudaMemsetAsync(out, 0, sizeof(int64_t), st));
+        if (total) CU(cudaMemsetAsync(total, 0, sizeof(long long), st));
+        return MM_OK;
+    }
+    int64_t* own = nullptr;
+    if (!scratch) {
+        CU(cudaMallocAsync((void**)&own, scan_scratch_elems(n) * sizeof(int64_t), st));
+        scratch = own;
+    }
+    int rc = scan_impl(counts, n, out + 1, st, scratch, 1, bounds_off, flag, total);
+    if (own) cudaFreeAsync(own, st);
     return rc;
 }
 
@@ -197,6 +215,36 @@ int validate(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* 
         if (plan->semiring == MM_SR_ARITHMETIC && bt->nnz && !bt->values)
             return fail(MM_ERR_INPUT, "plus-times needs B^T values");
     }
+    return MM_OK;
+}
+
+// Resident blocks per SM of a kernel at a launch shape.  The dynamic
+// shared-memory attribute and the occupancy query are host API calls worth a
+// few microseconds each, so results are cached per (kernel, threads, smem).
+struct OccEntry {
+    const void* fn;
+    int threads;
+    size_t smem;
+    int occ;
+};
+thread_local std::vector<OccEntry> g_occ_cache;
+thread_local std::vector<std::pair<const void*, size_t>> g_smem_attr;
+
+int kernel_occupancy(const void* fn, int threads, size_t smem, int* occ) {
+    for (const OccEntry& e : g_occ_cache)
+        if (e.fn == fn && e.threads == threads && e.smem == smem) { *occ = e.occ; return MM_OK; }
+    size_t* have = nullptr;
+    for (auto& a : g_smem_attr)
+        if (a.first == fn) have = &a.second;
+    if (!have) { g_smem_attr.push_back({fn, 0}); have = &g_smem_attr.back().second; }
+    if (smem > *have) {
+        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        *have = smem;
+    }
+    int o = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
+    g_occ_cache.push_back({fn, threads, smem, o});
+    *occ = o;
     return MM_OK;
 }
 
@@ -275,7 +323,8 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
 
 int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order, int norder) {
     cudaStream_t main_st = h->stream;
-    const bool concurrent = norder > 1;
+    // small multiplies: forking costs more host time than the overlap saves
+    const bool concurrent = norder > 1 && h->sum.gen_flops >= (1ull << 22);
     if (concurrent) {
         if (!h->fork_ev) {
             CU(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
@@ -287,7 +336,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
         CU(cudaEventRecord(h->fork_ev, main_st));
         for (int q = 0; q < mm_handle::NAUX && q < norder; q++) CU(cudaStreamWaitEvent(h->aux[q], h->fork_ev, 0));
     }
-    int32_t* cursors = h->cursors + (numeric ? NBINS : 0);
+    int rc = MM_OK;
+    int32_t* cursors = h->cursors + (numeric ? 2 * NBINS : NBINS);
     for (int oi = 0; oi < norder; oi++) {
         const int b = order[oi];
         const int cnt = h->sum.bin_count[b];
@@ -304,9 +354,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             else if (kind == 0) kern = k_pull_inner<0, true>;
             else if (kind == 1) kern = k_pull_inner<1, true>;
             else kern = k_pull_inner<2, true>;
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
             int grid = std::max(1, std::min((cnt + 7) / 8, std::max(occ, 1) * h->num_sms));
             ++g_launches;
             kern<<<grid, 256, smem, st>>>(h->prob, out, wk, stage);
@@ -331,9 +380,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             size_t queue = kind == 2 ? 0 : (size_t)64 * (kind == 1 ? 24 : 8);
             size_t smem = (smem_table ? groups * table : 0) + groups * batch + (threads / 32) * queue;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "hash tier table exceeds shared memory");
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            if ((rc = kernel_occupancy((const void*)kern, threads, smem, &occ))) return rc;
             int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
             unsigned char* gslab = nullptr;
             if (!smem_table) {
@@ -365,9 +413,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             const size_t batch = batch_bytes_rt(gw, kind);
             const size_t smem = (smem_region ? groups * rb : 0) + groups * batch;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "rank tier region exceeds shared memory");
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            if ((rc = kernel_occupancy((const void*)kern, threads, smem, &occ))) return rc;
             const int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
             unsigned char* gslab = nullptr;
             if (!smem_region) {
@@ -402,9 +449,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             const size_t wbytes = comp_rows ? 0 : (((size_t)(kind == 0 ? 4 : 12) * nm_max + 15) & ~(size_t)15);
             const bool in_smem = sub == 0;
             const size_t smem = in_smem ? 8 * wbytes : 0;
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
             const int grid = std::max(1, std::min((cnt + 7) / 8, std::max(occ, 1) * h->num_sms));
             unsigned char* gslab = nullptr;
             if (!in_smem && !comp_rows) {
@@ -436,9 +482,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             const size_t batch = batch_bytes_rt(gw, kind);
             const size_t smem = groups * (rb + batch);
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "dense MSA window exceeds shared memory");
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
             const int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
             if (debug_launches())
                 fprintf(stderr, "[mm] dense-msa bin %d rows %d gw %d words %d smem %zu grid %d occ %d\n", b, cnt, gw,
@@ -472,9 +517,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             const size_t batch = batch_bytes_rt(gw, kind);
             const size_t smem = groups * (rb + batch);
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "sparse MSA region exceeds shared memory");
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
             const int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
             if (debug_launches())
                 fprintf(stderr, "[mm] sparse-msa bin %d rows %d gw %d dir %d blk %d nm %d smem %zu grid %d occ %d\n",
@@ -496,9 +540,8 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             // two 4-warp groups per block while the bitmaps fit, else one group
             const size_t smem = 2 * 4 * (size_t)words_max;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "single-entry bitmap exceeds shared memory");
-            CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem));
+            if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
             const int grid = std::max(1, std::min((cnt + 1) / 2, std::max(occ, 1) * h->num_sms));
             ++g_launches;
             kern<<<grid, 256, smem, st>>>(h->prob, out, wk, words_max);
@@ -577,33 +620,48 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     ap.has_bt = use_bt;
     const int64_t m = h->nrows;
 
-    if ((rc = dalloc(h, &h->d_summary, 1))) return rc;
-    if ((rc = dalloc(h, &h->row_flops, m))) return rc;
-    p.row_flops = h->row_flops;
-    if ((rc = dalloc(h, &h->row_bin, m))) return rc;
-    if ((rc = dalloc(h, &h->row_cap_lg, m))) return rc;
-    if ((rc = dalloc(h, &h->rows_list, m))) return rc;
-    if ((rc = dalloc(h, &h->cursors, 2 * NBINS))) return rc;
-    if ((rc = dalloc(h, &h->d_bin_off, NBINS + 1))) return rc;
-    if ((rc = dalloc(h, &h->row_nnz, m))) return rc;
-    if ((rc = dalloc(h, &h->c_row_ptr, m + 1))) return rc;
+    // One pool allocation carves every per-multiply array; summary and fetch
+    // cursors sit together at the front so a single memset clears both.
     const bool need_bound = comp && plan->phases == 1 && !symbolic_only;
-    if (need_bound) {
-        if ((rc = dalloc(h, &h->bound, m))) return rc;
-        if ((rc = dalloc(h, &h->bound_ptr, m + 1))) return rc;
-    } else {
-        h->bound = nullptr;
-        h->bound_ptr = nullptr;
-    }
-    CU(cudaMemsetAsync(h->d_summary, 0, sizeof(Summary), st));
-    CU(cudaMemsetAsync(h->cursors, 0, 2 * NBINS * sizeof(int32_t), st));
-    if (m > 0) CU(cudaMemsetAsync(h->row_nnz, 0, m * sizeof(int64_t), st));
+    const bool plain_1p = !comp && plan->phases == 1 && !symbolic_only;
+    const int64_t scan_elems = scan_scratch_elems(m);
+    size_t off = 0;
+    auto carve = [&](size_t bytes) { size_t at = off; off += (bytes + 255) & ~(size_t)255; return at; };
+    const size_t o_sum = carve(sizeof(Summary) + 3 * NBINS * sizeof(int32_t));
+    const size_t o_flops = carve(m * sizeof(int64_t));
+    const size_t o_nnz = carve(m * sizeof(int64_t));
+    const size_t o_ptr = carve((m + 1) * sizeof(int64_t));
+    const size_t o_bound = need_bound ? carve(m * sizeof(int64_t)) : 0;
+    const size_t o_bptr = need_bound ? carve((m + 1) * sizeof(int64_t)) : 0;
+    const size_t o_scan = carve(scan_elems * sizeof(int64_t));
+    const size_t o_rows = carve(m * sizeof(int32_t));
+    const size_t o_bin = carve(m);
+    const size_t o_cap = carve(m);
+    const size_t o_tidx = plain_1p ? carve(mask->nnz * sizeof(int32_t)) : 0;
+    const size_t o_tval = plain_1p ? carve(mask->nnz * 8) : 0;
+    unsigned char* slab = nullptr;
+    if ((rc = dalloc(h, &slab, off))) return rc;
+    h->d_summary = (Summary*)(slab + o_sum);
+    h->cursors = (int32_t*)(slab + o_sum + sizeof(Summary));
+    h->row_flops = (int64_t*)(slab + o_flops);
+    h->row_nnz = (int64_t*)(slab + o_nnz);
+    h->c_row_ptr = (int64_t*)(slab + o_ptr);
+    h->bound = need_bound ? (int64_t*)(slab + o_bound) : nullptr;
+    h->bound_ptr = need_bound ? (int64_t*)(slab + o_bptr) : nullptr;
+    h->scan_scratch = (int64_t*)(slab + o_scan);
+    h->rows_list = (int32_t*)(slab + o_rows);
+    h->row_bin = (uint8_t*)(slab + o_bin);
+    h->row_cap_lg = (int8_t*)(slab + o_cap);
+    h->tmp_idx = plain_1p ? (int32_t*)(slab + o_tidx) : nullptr;
+    h->tmp_val = plain_1p ? (void*)(slab + o_tval) : nullptr;
+    p.row_flops = h->row_flops;
+    CU(cudaMemsetAsync(h->d_summary, 0, sizeof(Summary) + 3 * NBINS * sizeof(int32_t), st));
 
     if (m > 0) {
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
         ++g_launches;
         k_analyze<<<grid, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin, h->row_cap_lg,
-                                        h->d_summary);
+                                        h->d_summary, symbolic_only ? nullptr : h->row_nnz);
         CU(cudaGetLastError());
     }
     if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
@@ -616,15 +674,11 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     h->stats.rows_empty = h->sum.bin_count[BIN_EMPTY];
     h->stats.rows_pull = h->sum.bin_count[BIN_PULL];
     h->stats.rows_push = m - h->stats.rows_empty - h->stats.rows_pull;
-    if (m > 0) {
-        CU(cudaMemcpyAsync(h->d_bin_off, h->bin_off, (NBINS + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-        // the pinned copy of bin_off must stay alive until the copy runs: bin_off
-        // lives in the handle, which outlives the stream work
+    if (m > 0 && h->stats.rows_empty < m) {
         int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8);
         ++g_launches;
-        k_bin_scatter<<<grid, 256, 0, st>>>(m, h->row_bin, h->d_bin_off, h->cursors, h->rows_list);
+        k_bin_scatter<<<grid, 256, 0, st>>>(m, h->row_bin, h->d_summary, h->cursors, h->rows_list);
         CU(cudaGetLastError());
-        CU(cudaMemsetAsync(h->cursors, 0, 2 * NBINS * sizeof(int32_t), st));
     }
     mark(h, 2);
 
@@ -637,8 +691,10 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
             CU(cudaStreamSynchronize(st));
             return MM_OK;
         }
-        if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st))) return rc;
-        if ((rc = sync_read(h, h->h_scalar, h->c_row_ptr + m, sizeof(long long)))) return rc;
+        if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st, h->scan_scratch, nullptr, nullptr,
+                                 &h->d_summary->total_nnz)))
+            return rc;
+        if ((rc = sync_read(h, h->h_scalar, &h->d_summary->total_nnz, sizeof(long long)))) return rc;
         h->total_nnz = *h->h_scalar;
         mark(h, 4);
         *out_nnz = h->total_nnz;
@@ -647,20 +703,17 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     }
 
     // ---- one-phase: bounded numeric into slots, then exact row pointer ----
-    int64_t tmp_total;
     if (comp) {
-        if ((rc = exclusive_scan(h->bound, m, h->bound_ptr, st))) return rc;
+        if ((rc = exclusive_scan(h->bound, m, h->bound_ptr, st, h->scan_scratch))) return rc;
         h->bound_off = h->bound_ptr;
-        tmp_total = (int64_t)h->sum.bound_total;
+        const int64_t tmp_total = (int64_t)h->sum.bound_total;
+        if ((rc = dalloc(h, &h->tmp_idx, tmp_total))) return rc;
+        unsigned char* tv = nullptr;
+        if ((rc = dalloc(h, &tv, (size_t)tmp_total * 8))) return rc;
+        h->tmp_val = tv;
     } else {
         h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
-        tmp_total = mask->nnz;
     }
-    if ((rc = dalloc(h, &h->tmp_idx, tmp_total))) return rc;
-    void* tv = nullptr;
-    CU(cudaMallocAsync(&tv, std::max<size_t>(tmp_total * 8, 16), st));
-    h->allocs.push_back(tv);
-    h->tmp_val = tv;
     Out o{};
     o.off = h->bound_off;
     o.idx = h->tmp_idx;
@@ -670,15 +723,11 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     o.out_f64 = h->out_f64;
     if ((rc = launch_bins(h, true, o))) return rc;
     mark(h, 3);
-    if (m > 0) {
-        // the bound assertion (multiply.py:390) rides on the nnz readback below
-        int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8);
-        ++g_launches;
-        k_check_bounds<<<grid, 256, 0, st>>>(m, h->row_nnz, h->bound_off, &h->d_summary->flag);
-    }
-    if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st))) return rc;
-    CU(cudaMemcpyAsync(&h->d_summary->total_nnz, h->c_row_ptr + m, sizeof(long long),
-                       cudaMemcpyDeviceToDevice, st));
+    // the bound assertion (multiply.py:390) is folded into the scan and rides
+    // on the nnz readback below
+    if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st, h->scan_scratch, h->bound_off,
+                             &h->d_summary->flag, &h->d_summary->total_nnz)))
+        return rc;
     if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
     h->total_nnz = h->h_summary->total_nnz;
     h->stats.evaluated_multiplies = (int64_t)h->h_summary->evaluated;
@@ -894,7 +943,7 @@ int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops,
     if (a->nrows > 0) {
         int grid = (int)std::min<int64_t>((a->nrows + 255) / 256, 148 * 8);
         ++g_launches;
-        k_analyze<<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s);
+        k_analyze<<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr);
     }
     if (total) CU(cudaMemcpyAsync(total, &s->gen_flops, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     cudaFreeAsync(s, st);

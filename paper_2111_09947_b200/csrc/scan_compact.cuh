@@ -13,19 +13,29 @@ constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 // Block-local inclusive scan of `in` (n items) written to out[0..n);
-// each block's total goes to partials[blockIdx.x].
+// each block's total goes to partials[blockIdx.x].  Folded side jobs (so a
+// small scan is one launch): out[-1] = 0 when zero_prev (exclusive form),
+// the one-phase bound assertion (multiply.py:390) when bounds_off is given,
+// and the grand total into *total when the scan is a single tile.
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile(const int64_t* in, int64_t n,
-                                                            int64_t* out, int64_t* partials) {
+                                                            int64_t* out, int64_t* partials,
+                                                            int zero_prev, const int64_t* bounds_off,
+                                                            int* flag, long long* total) {
     __shared__ long long s_warp[32];
     const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    if (zero_prev && blockIdx.x == 0 && threadIdx.x == 0) out[-1] = 0;
     long long v[SCAN_ITEMS];
     long long run = 0;
+    bool over = false;
 #pragma unroll
     for (int q = 0; q < SCAN_ITEMS; q++) {
         int64_t idx = base + q;
-        run += idx < n ? in[idx] : 0;
+        const long long x = idx < n ? in[idx] : 0;
+        if (bounds_off && idx < n) over |= x > bounds_off[idx + 1] - bounds_off[idx];
+        run += x;
         v[q] = run;
     }
+    if (bounds_off && __any_sync(FULL, over) && (threadIdx.x & 31) == 0) atomicExch(flag, 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     long long x = run;
 #pragma unroll
@@ -51,13 +61,21 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile(const int64_t* in, i
         int64_t idx = base + q;
         if (idx < n) out[idx] = v[q] + prefix;
     }
-    if (threadIdx.x == SCAN_THREADS - 1) partials[blockIdx.x] = s_warp[31];
+    if (threadIdx.x == SCAN_THREADS - 1) {
+        partials[blockIdx.x] = s_warp[31];
+        if (total && gridDim.x == 1) *total = s_warp[31];
+    }
 }
 
-// out[i] += offsets[block of i] (offsets = exclusive scan of the partials).
-__global__ void k_scan_add(int64_t* out, int64_t n, const int64_t* offsets) {
+// out[i] += offsets[block of i] (offsets = exclusive scan of the partials);
+// the last element's final value also goes to *total when given.
+__global__ void k_scan_add(int64_t* out, int64_t n, const int64_t* offsets, long long* total) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx < n) out[idx] += offsets[idx / SCAN_TILE];
+    if (idx < n) {
+        const int64_t v = out[idx] + offsets[idx / SCAN_TILE];
+        out[idx] = v;
+        if (total && idx == n - 1) *total = v;
+    }
 }
 
 __global__ void k_set_zero_i64(int64_t* p) { *p = 0; }

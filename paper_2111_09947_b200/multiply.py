@@ -178,10 +178,15 @@ def multiply_device(mask: DeviceCsr, a: DeviceCsr, b: DeviceCsr, plan: MultiplyP
         _raise(rc)
     t1 = time.perf_counter()
     n = int(nnz.value)
-    with torch.cuda.stream(stream):
+    if stream == torch.cuda.current_stream(dev):
         row_ptr = torch.empty(mask.nrows + 1, dtype=torch.int64, device=dev)
         col_idx = torch.empty(n, dtype=torch.int32, device=dev)
         values = torch.empty(n, dtype=dtype, device=dev)
+    else:
+        with torch.cuda.stream(stream):
+            row_ptr = torch.empty(mask.nrows + 1, dtype=torch.int64, device=dev)
+            col_idx = torch.empty(n, dtype=torch.int32, device=dev)
+            values = torch.empty(n, dtype=dtype, device=dev)
     st = _lib.StatsT()
     rc = lib.mm_multiply_end(h, row_ptr.data_ptr(), col_idx.data_ptr() if n else None,
                              values.data_ptr() if n else None, C.byref(st))
