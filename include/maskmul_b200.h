@@ -181,6 +181,39 @@ int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32
  * count reduction of triangle_count (graphs.py:96). */
 int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* stream);
 
+/* ---- element-wise building blocks of the graph drivers (graphs.py:121-200) ---- */
+
+/* lookup_rows (_kernels.py:597-612): for every stored entry t of X (row i,
+ * column j), out[t] = Y[i, j] and found[t] = 1 when Y holds that entry, else
+ * out[t] = 0 and found[t] = 0 (graphs._values_at, graphs.py:121-129).  X and
+ * Y canonical, same shape; dtype MM_DTYPE_* of Y's values; found may be NULL. */
+int mm_lookup_rows(const mm_matrix_t* x, const mm_matrix_t* y, int dtype, void* out, uint8_t* found,
+                   void* stream);
+
+/* Betweenness-centrality dependency weights on sigma_t's pattern
+ * (graphs.py:181-184): w[t] = (1 + delta[i,j]) / paths[i,j], absent delta
+ * entries reading 0.  float64. */
+int mm_bc_dependency_weights(const mm_matrix_t* sigma_t, const mm_matrix_t* delta, const mm_matrix_t* paths,
+                             double* w, void* stream);
+
+/* out[t] = x.values[t] * paths[i,j] on x's pattern (graphs.py:186). float64. */
+int mm_bc_scale_by(const mm_matrix_t* x, const mm_matrix_t* paths, double* out, void* stream);
+
+/* ewise_add (sparse.py:360-370), two calls like the multiply: begin writes
+ * the union's row pointer into c_row_ptr[nrows+1] (device) and its nnz into
+ * *nnz (host; synchronous on `stream`); end fills c_idx / c_val (device,
+ * nnz entries), values added where both operands hold an entry. */
+int mm_ewise_add_begin(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* c_row_ptr, int64_t* nnz,
+                       void* stream);
+int mm_ewise_add_end(const mm_matrix_t* a, const mm_matrix_t* b, int dtype, const int64_t* c_row_ptr,
+                     int32_t* c_idx, void* c_val, void* stream);
+
+/* BC score update for one source batch (graphs.py:188-197): for every row r,
+ * scores[r] += delta[r, :] summed in column order, then, when src_col[r] >= 0
+ * (r is the batch's source in column src_col[r]), scores[r] -= delta[r,
+ * src_col[r]] (0 when absent).  src_col may be NULL (no sources). */
+int mm_bc_accumulate(const mm_matrix_t* delta, const int32_t* src_col, double* scores, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

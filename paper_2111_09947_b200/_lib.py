@@ -19,7 +19,9 @@ MM_DTYPE_INT64, MM_DTYPE_FLOAT64 = 0, 1
 EXPORTS = ("mm_abi_version", "mm_last_error", "mm_create", "mm_destroy", "mm_multiply_begin",
            "mm_multiply_end", "mm_symbolic", "mm_row_flops", "mm_exclusive_scan",
            "mm_compact_rows", "mm_reduce_sum", "mm_profile_enable", "mm_profile_read",
-           "mm_profile_bins", "mm_set_tuning", "mm_filter_min")
+           "mm_profile_bins", "mm_set_tuning", "mm_filter_min", "mm_lookup_rows",
+           "mm_bc_dependency_weights", "mm_bc_scale_by", "mm_ewise_add_begin", "mm_ewise_add_end",
+           "mm_bc_accumulate")
 
 
 class MatrixT(C.Structure):
@@ -68,6 +70,12 @@ def load(path: str | None = None):
     lib.mm_profile_bins.argtypes = [P, P, P, C.c_int]
     lib.mm_set_tuning.argtypes = [P, P, C.c_int]
     lib.mm_filter_min.argtypes = [C.POINTER(MatrixT), C.c_int64, P, P, C.POINTER(C.c_int64), P]
+    lib.mm_lookup_rows.argtypes = [PM, PM, C.c_int, P, P, P]
+    lib.mm_bc_dependency_weights.argtypes = [PM, PM, PM, P, P]
+    lib.mm_bc_scale_by.argtypes = [PM, PM, P, P]
+    lib.mm_ewise_add_begin.argtypes = [PM, PM, P, C.POINTER(C.c_int64), P]
+    lib.mm_ewise_add_end.argtypes = [PM, PM, C.c_int, P, P, P, P]
+    lib.mm_bc_accumulate.argtypes = [PM, P, P, P]
     for name in EXPORTS:
         getattr(lib, name)
         if name not in ("mm_last_error",):

@@ -27,6 +27,7 @@
 #include "push_msa_sparse.cuh"
 #include "push_dense.cuh"
 #include "scan_compact.cuh"
+#include "graph_ops.cuh"
 
 using namespace mm;
 
@@ -1037,4 +1038,120 @@ int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* str
     return MM_OK;
 }
 
+// ---- element-wise graph building blocks (graph_ops.cuh) ----
+
+static int warp_grid(int64_t rows) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((rows + 7) / 8, (int64_t)148 * 16));
+}
+
+int mm_lookup_rows(const mm_matrix_t* x, const mm_matrix_t* y, int dtype, void* out, uint8_t* found,
+                   void* stream) {
+    if (!x || !y || (x->nnz > 0 && !out)) return fail(MM_ERR_INPUT, "null argument");
+    if (x->nrows != y->nrows || x->ncols != y->ncols) return fail(MM_ERR_INPUT, "lookup_rows: shape mismatch");
+    if (x->nnz == 0 || x->nrows == 0) return MM_OK;
+    if (y->nnz > 0 && !y->values) return fail(MM_ERR_INPUT, "lookup_rows: Y needs values");
+    cudaStream_t st = (cudaStream_t)stream;
+    ++g_launches;
+    if (dtype == MM_DTYPE_FLOAT64)
+        k_lookup<LK_VALUE, double><<<warp_grid(x->nrows), 256, 0, st>>>(
+            x->nrows, x->ptr, x->idx, nullptr, y->ptr, y->idx, (const double*)y->values, nullptr, nullptr, nullptr,
+            (double*)out, found);
+    else
+        k_lookup<LK_VALUE, long long><<<warp_grid(x->nrows), 256, 0, st>>>(
+            x->nrows, x->ptr, x->idx, nullptr, y->ptr, y->idx, (const long long*)y->values, nullptr, nullptr,
+            nullptr, (long long*)out, found);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+int mm_bc_dependency_weights(const mm_matrix_t* sigma, const mm_matrix_t* delta, const mm_matrix_t* paths,
+                             double* w, void* stream) {
+    if (!sigma || !delta || !paths || (sigma->nnz > 0 && !w)) return fail(MM_ERR_INPUT, "null argument");
+    if (sigma->nrows != delta->nrows || sigma->nrows != paths->nrows)
+        return fail(MM_ERR_INPUT, "bc weights: row count mismatch");
+    if (sigma->nnz == 0) return MM_OK;
+    ++g_launches;
+    k_lookup<LK_BC_WEIGHT, double><<<warp_grid(sigma->nrows), 256, 0, (cudaStream_t)stream>>>(
+        sigma->nrows, sigma->ptr, sigma->idx, nullptr, delta->ptr, delta->idx, (const double*)delta->values,
+        paths->ptr, paths->idx, (const double*)paths->values, w, nullptr);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+int mm_bc_scale_by(const mm_matrix_t* x, const mm_matrix_t* paths, double* out, void* stream) {
+    if (!x || !paths || (x->nnz > 0 && (!out || !x->values))) return fail(MM_ERR_INPUT, "null argument");
+    if (x->nrows != paths->nrows) return fail(MM_ERR_INPUT, "bc scale: row count mismatch");
+    if (x->nnz == 0) return MM_OK;
+    ++g_launches;
+    k_lookup<LK_SCALE, double><<<warp_grid(x->nrows), 256, 0, (cudaStream_t)stream>>>(
+        x->nrows, x->ptr, x->idx, (const double*)x->values, paths->ptr, paths->idx, (const double*)paths->values,
+        nullptr, nullptr, nullptr, out, nullptr);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+int mm_ewise_add_begin(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* c_row_ptr, int64_t* nnz, void* stream) {
+    if (!a || !b || !c_row_ptr || !nnz) return fail(MM_ERR_INPUT, "null argument");
+    if (a->nrows != b->nrows || a->ncols != b->ncols)
+        return fail(MM_ERR_INPUT, "shape mismatch (" + std::to_string(a->nrows) + ", " + std::to_string(a->ncols) +
+                                      ") vs (" + std::to_string(b->nrows) + ", " + std::to_string(b->ncols) + ")");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t m = a->nrows;
+    int64_t* counts = nullptr;
+    long long* total = nullptr;
+    CU(cudaMallocAsync((void**)&counts, (std::max<int64_t>(m, 1) + 2) * sizeof(int64_t), st));
+    total = (long long*)(counts + std::max<int64_t>(m, 1));
+    if (m > 0) {
+        ++g_launches;
+        k_ewise_count<<<warp_grid(m), 256, 0, st>>>(m, a->ptr, a->idx, b->ptr, b->idx, counts);
+    }
+    int rc = exclusive_scan(counts, m, c_row_ptr, st, nullptr, nullptr, nullptr, total);
+    long long* h = nullptr;
+    if (!rc) {
+        cudaError_t e = cudaMallocHost((void**)&h, sizeof(long long));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, total, sizeof(long long), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = fail(MM_ERR_CUDA, std::string("ewise_add count readback: ") + cudaGetErrorString(e));
+        else *nnz = *h;
+    }
+    if (h) cudaFreeHost(h);
+    cudaFreeAsync(counts, st);
+    return rc;
+}
+
+int mm_ewise_add_end(const mm_matrix_t* a, const mm_matrix_t* b, int dtype, const int64_t* c_row_ptr,
+                     int32_t* c_idx, void* c_val, void* stream) {
+    if (!a || !b || !c_row_ptr) return fail(MM_ERR_INPUT, "null argument");
+    if (a->nrows != b->nrows || a->ncols != b->ncols) return fail(MM_ERR_INPUT, "shape mismatch");
+    if ((a->nnz && !a->values) || (b->nnz && !b->values)) return fail(MM_ERR_INPUT, "ewise_add needs values");
+    if ((a->nnz || b->nnz) && (!c_idx || !c_val)) return fail(MM_ERR_INPUT, "output arrays required");
+    const int64_t m = a->nrows;
+    if (m == 0 || (a->nnz == 0 && b->nnz == 0)) return MM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    ++g_launches;
+    if (dtype == MM_DTYPE_FLOAT64)
+        k_ewise_fill<double><<<warp_grid(m), 256, 0, st>>>(m, a->ptr, a->idx, (const double*)a->values, b->ptr,
+                                                           b->idx, (const double*)b->values, c_row_ptr, c_idx,
+                                                           (double*)c_val);
+    else
+        k_ewise_fill<long long><<<warp_grid(m), 256, 0, st>>>(m, a->ptr, a->idx, (const long long*)a->values,
+                                                              b->ptr, b->idx, (const long long*)b->values,
+                                                              c_row_ptr, c_idx, (long long*)c_val);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+int mm_bc_accumulate(const mm_matrix_t* delta, const int32_t* src_col, double* scores, void* stream) {
+    if (!delta || !scores || (delta->nnz > 0 && !delta->values)) return fail(MM_ERR_INPUT, "null argument");
+    const int64_t m = delta->nrows;
+    if (m == 0) return MM_OK;
+    ++g_launches;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)148 * 16));
+    k_bc_accumulate<<<grid, 256, 0, (cudaStream_t)stream>>>(m, delta->ptr, delta->idx, (const double*)delta->values,
+                                                             src_col, scores);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
 }  // extern "C"
+

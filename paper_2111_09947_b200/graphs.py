@@ -2,7 +2,10 @@
 
 triangle_count mirrors pkg/src/maskmul/graphs.py:87-96 (relabel by degree,
 strict lower triangle L, C = L (.) (L L) under plus-pair int64, sum(C));
-k_truss mirrors graphs.py:99-118 (support = G (.) (G G), prune < k-2, repeat).
+k_truss mirrors graphs.py:99-118 (support = G (.) (G G), prune < k-2, repeat);
+betweenness_centrality mirrors graphs.py:136-200 (batched Brandes: forward
+frontier expansion with a complemented mask, backward dependency
+accumulation with a plain mask), every step on the device.
 Graph preparation stays on the host as in the reference (it is excluded from
 the timings there too); every multiply and the final reduction run on the GPU.
 """
@@ -10,14 +13,30 @@ the timings there too); every multiply and the final reduction run on the GPU.
 from __future__ import annotations
 
 from dataclasses import dataclass, field, replace
+from typing import Sequence
 
 import numpy as np
 
 from .device import DeviceCsr
-from .multiply import MultiplyPlan, multiply_device, reduce_sum
-from .semiring import plus_pair_semiring
+from .multiply import MultiplyPlan, PlanError, multiply_device, reduce_sum
+from .semiring import arithmetic_semiring, plus_pair_semiring
 from .sparse import (CsrMatrix, SparseError, degree_sort_relabel, from_arrays,
                      is_pattern_symmetric, tril_strict)
+
+
+@dataclass(frozen=True)
+class BcConfig:
+    """graphs.py:26-38."""
+    batch_size: int = 512
+    sources: Sequence[int] | None = None  # None: every vertex is a source
+
+    def __post_init__(self):
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        if self.sources is not None:
+            src = list(self.sources)
+            if len(set(src)) != len(src):
+                raise ValueError("sources must be distinct")
 
 
 @dataclass
@@ -97,4 +116,83 @@ def k_truss(g: CsrMatrix, k: int, plan: MultiplyPlan, device=None) -> KernelResu
     host = cur.to_host()
     host.values = np.ones(host.nnz, dtype=np.int64)
     res.value = host
+    return res
+
+
+def _record(res: KernelResult, st) -> None:
+    res.multiply_seconds += st.total_seconds
+    res.flops += st.generated_flops
+    res.evaluated += st.evaluated_multiplies
+    res.multiplies += 1
+    res.per_multiply.append((st.total_seconds, st.generated_flops))
+
+
+def betweenness_centrality(g: CsrMatrix, cfg: BcConfig, plan: MultiplyPlan, device=None) -> KernelResult:
+    """Batched multi-source Brandes over masked multiplies (graphs.py:136-200).
+
+    Forward: next = not(paths) (.) (A^T frontier) under plus-times float64,
+    paths += next, until the frontier is empty.  Backward, level by level:
+    w = (1 + delta) / paths on the level's pattern, wq = prev_level (.) (A w),
+    delta += wq * paths.  Scores add each batch's delta rows and drop a
+    source's own entry.  Everything after the graph upload stays in HBM; one
+    nnz readback per multiply / union decides sizes.  Unnormalised, directed
+    convention summed over the sources, like the reference.
+    """
+    import torch
+
+    from . import elementwise as ew
+
+    if plan.algorithm in ("mca", "inner"):
+        raise PlanError(f"{plan.algorithm} does not support the complemented "
+                        "masked multiplies betweenness centrality needs")
+    if g.nrows != g.ncols:
+        raise SparseError("betweenness centrality requires a square adjacency matrix")
+    n = g.nrows
+    sources = (np.arange(n, dtype=np.int64) if cfg.sources is None
+               else np.asarray(list(cfg.sources), dtype=np.int64))
+    if sources.size and (sources.min() < 0 or sources.max() >= n):
+        raise SparseError("source vertex out of range")
+    sem = arithmetic_semiring(np.float64)
+    fwd_plan = replace(plan, semiring=sem, complemented=True)
+    bwd_plan = replace(plan, semiring=sem, complemented=False)
+    adj = DeviceCsr.from_host(g, dtype=np.float64, device=device)
+    dev = adj.idx.device
+    t = adj.transpose_storage()          # A^T as CSR, hoisted once (graphs.py:160)
+    adj_t = DeviceCsr(n, n, t.ptr, t.idx, t.values)
+    res = KernelResult(None)
+    scores = torch.zeros(n, dtype=torch.float64, device=dev)
+    src_col = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    for lo in range(0, sources.size, cfg.batch_size):
+        batch = sources[lo: lo + cfg.batch_size]
+        b = int(batch.size)
+        order = np.argsort(batch, kind="stable")
+        ptr = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(ptr, batch + 1, 1)
+        sigma = DeviceCsr(n, b, torch.from_numpy(np.cumsum(ptr)).to(dev),
+                          torch.from_numpy(order.astype(np.int32)).to(dev),
+                          torch.ones(b, dtype=torch.float64, device=dev))
+        paths = sigma
+        frontiers = [sigma]
+        while True:
+            nxt, st = multiply_device(paths, adj_t, frontiers[-1], fwd_plan, complemented=True)
+            _record(res, st)
+            if nxt.nnz == 0:
+                break
+            paths = ew.ewise_add(paths, nxt)
+            frontiers.append(nxt)
+        delta = DeviceCsr(n, b, torch.zeros(n + 1, dtype=torch.int64, device=dev),
+                          torch.empty(0, dtype=torch.int32, device=dev),
+                          torch.empty(0, dtype=torch.float64, device=dev))
+        for lvl in range(len(frontiers) - 1, 0, -1):
+            sig_t, sig_prev = frontiers[lvl], frontiers[lvl - 1]
+            w = DeviceCsr(n, b, sig_t.ptr, sig_t.idx, ew.bc_dependency_weights(sig_t, delta, paths))
+            wq, st = multiply_device(sig_prev, adj, w, bwd_plan)
+            _record(res, st)
+            contrib = DeviceCsr(n, b, wq.ptr, wq.idx, ew.bc_scale_by(wq, paths))
+            delta = ew.ewise_add(delta, contrib)
+        bt = torch.from_numpy(batch).to(dev)
+        src_col[bt] = torch.arange(b, dtype=torch.int32, device=dev)
+        ew.bc_accumulate(delta, src_col, scores)
+        src_col[bt] = -1
+    res.value = scores.cpu().numpy()
     return res

@@ -9,6 +9,7 @@ fixtures that the oracle and the CUDA path are pinned against.
         python tests/golden/make_golden.py            # KATs, random cases, cfg1-4
     ... make_golden.py --cfg2                          # R-MAT s20 triangle count (~1 min)
     ... make_golden.py --cfg5                          # R-MAT s22 k-truss support (~8 min)
+    ... make_golden.py --bc                            # betweenness centrality scores
 
 Digest convention (shared with tests/golden_util.py): sha256 over the
 little-endian bytes of int64 row_ptr, then int64 col_idx[:nnz], then the values
@@ -277,11 +278,89 @@ def cfg5():
                    MultiplyPlan(semiring=plus_pair_semiring(np.int64)))
 
 
+
+# ---------------------------------------------------------------------------
+# Betweenness centrality (graphs.py:136-200), SURVEY §8(f) row 2
+# ---------------------------------------------------------------------------
+
+def _bc_graph(spec):
+    """Graph recipes of the reference's BC tests (pkg/tests/test_graphs.py:110-170,
+    test_acceptance.py:139-152) and two larger R-MAT instances."""
+    from maskmul.graphs import BcConfig  # noqa: F401
+    kind = spec["graph"]
+    if kind == "path":
+        edges = []
+        for i in range(spec["n"] - 1):
+            edges += [(i, i + 1, 1), (i + 1, i, 1)]
+        return from_triples(spec["n"], spec["n"], edges)
+    if kind == "star":
+        edges = []
+        for i in range(1, spec["leaves"] + 1):
+            edges += [(0, i, 1), (i, 0, 1)]
+        return from_triples(spec["leaves"] + 1, spec["leaves"] + 1, edges)
+    if kind == "disconnected":
+        return from_triples(4, 4, [(0, 1, 1), (1, 0, 1), (2, 3, 1), (3, 2, 1)])
+    if kind == "random":   # test_graphs.random_graph with the rng fixture (conftest.py:48-49)
+        rng = np.random.default_rng(spec["seed"])
+        return simple_undirected_graph(random_csr(rng, spec["n"], spec["n"], spec["degree"]))
+    if kind == "rmat":
+        return simple_undirected_graph(generate(GeneratorSpec("rmat", spec["scale"], spec["ef"],
+                                                              seed=spec["seed"])))
+    raise ValueError(kind)
+
+
+BC_CASES = [
+    {"graph": "path", "n": 3, "batch": 2, "plans": ["msa"]},
+    {"graph": "path", "n": 4, "batch": 2, "plans": ["heap"]},
+    {"graph": "star", "leaves": 4, "batch": 3, "plans": ["msa"]},
+    {"graph": "star", "leaves": 4, "batch": 4, "plans": ["msa"]},
+    {"graph": "disconnected", "batch": 4, "plans": ["msa"]},
+    {"graph": "rmat", "scale": 6, "ef": 4, "seed": 5, "batch": 16, "plans": ["msa", "hash", "heap"]},
+    {"graph": "random", "n": 24, "degree": 3, "seed": 20240811, "batch": 3, "sources": [0, 3, 7, 11],
+     "plans": ["msa"]},
+    {"graph": "random", "n": 20, "degree": 3, "seed": 20240811, "batch": 1, "plans": ["msa"]},
+    {"graph": "random", "n": 20, "degree": 3, "seed": 20240811, "batch": 20, "plans": ["msa"]},
+    {"graph": "random", "n": 30, "degree": 4, "seed": 20240811, "batch": 8, "plans": ["hash"]},
+    {"graph": "rmat", "scale": 8, "ef": 4, "seed": 11, "batch": 64, "plans": ["msa"]},
+    {"graph": "rmat", "scale": 10, "ef": 8, "seed": 3, "batch": 128, "n_sources": 256, "source_seed": 7,
+     "plans": ["msa", "hash"]},
+]
+
+
+def make_bc():
+    from maskmul.graphs import BcConfig, betweenness_centrality
+    out = []
+    for spec in BC_CASES:
+        g = _bc_graph(spec)
+        sources = spec.get("sources")
+        if "n_sources" in spec:
+            sources = [int(x) for x in np.random.default_rng(spec["source_seed"]).choice(
+                g.nrows, spec["n_sources"], replace=False)]
+        rec = dict(spec)
+        rec["sources"] = sources
+        rec["digest_graph"] = digest_mat(g)
+        rec["results"] = {}
+        for algo in spec["plans"]:
+            t0 = time.perf_counter()
+            res = betweenness_centrality(g, BcConfig(batch_size=spec["batch"], sources=sources),
+                                         MultiplyPlan(algorithm=algo))
+            rec["results"][algo] = {
+                "scores_hex": [float(x).hex() for x in res.value],
+                "multiplies": res.multiplies, "flops": int(res.flops), "evaluated": int(res.evaluated),
+                "wall_seconds": time.perf_counter() - t0,
+            }
+        print("bc", {k: v for k, v in rec.items() if k != "results"},
+              {a: (r["multiplies"], r["flops"]) for a, r in rec["results"].items()}, flush=True)
+        out.append(rec)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
     ap.add_argument("--cfg5", action="store_true")
     ap.add_argument("--small", action="store_true")
+    ap.add_argument("--bc", action="store_true")
     args = ap.parse_args()
     meta = {"numpy": np.__version__, "reference": "maskmul " + maskmul.__version__,
             "python": sys.version.split()[0]}
@@ -301,6 +380,9 @@ def main():
         cfgs["cfg1"] = cfg1()
         cfgs["cfg3"] = cfg3()
         cfgs["cfg4"] = cfg4()
+    if args.bc:
+        with open(os.path.join(HERE, "bc.json"), "w") as f:
+            json.dump({"meta": meta, "cases": make_bc()}, f)
     if args.cfg2:
         cfgs["cfg2"] = cfg2()
     if args.cfg5:

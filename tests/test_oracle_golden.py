@@ -122,3 +122,24 @@ def test_cfg3_cfg4_inputs_and_outputs():
                                workers=oracle.max_threads())
     assert digest_csr(r.row_ptr, r.col_idx, r.values) == g["digest_c"]
     assert r.evaluated_multiplies == g["evaluated"]
+
+
+def test_bc_oracle_matches_reference_scores_bitwise():
+    """oracle/bc.py (graphs.py:136-200 restated) against the reference's own
+    betweenness scores (tests/golden/bc.json), bit for bit, plus the reference's
+    multiply count, generated flops and evaluated products."""
+    from bc_cases import bc_cases, scores
+    from oracle.bc import betweenness_centrality as oracle_bc
+    n_checked = 0
+    for spec, g in bc_cases():
+        for algo, want in spec["results"].items():
+            got, count, flops, evaluated = oracle_bc(g, spec["batch"], spec["sources"], algorithm=algo)
+            ref = scores(want["scores_hex"])
+            assert (count, flops, evaluated) == (want["multiplies"], want["flops"], want["evaluated"]), spec
+            if algo == "heap":
+                # the reference's heap folds fp64 in tie order: same to 1e-12
+                np.testing.assert_allclose(got, ref, rtol=1e-12, atol=0)
+            else:
+                assert np.array_equal(got.view(np.int64), ref.view(np.int64)), (spec["graph"], algo)
+            n_checked += 1
+    assert n_checked >= 15
