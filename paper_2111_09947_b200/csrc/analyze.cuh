@@ -32,8 +32,10 @@ enum Bin : int {
     BIN_SINGLE = 35,  // one A entry: filtered, scaled copy of B_k (auto)
     BIN_MSAS0 = 36,   // + tier (0..2): MSA with a sparse two-level window bitmap
     BIN_MSAD0 = 39,   // + tier (0..2): MSA with a dense per-column window (push_dense.cuh)
-    NBINS = 42
+    BIN_MSADC0 = 42,  // + tier (0..2): complemented MSA over every column (narrow outputs)
+    NBINS = 45
 };
+__host__ __device__ constexpr bool is_msadc_bin(int b) { return b >= BIN_MSADC0 && b < BIN_MSADC0 + 3; }
 __host__ __device__ constexpr bool is_msas_bin(int b) { return b >= BIN_MSAS0 && b < BIN_MSAS0 + 3; }
 __host__ __device__ constexpr bool is_msad_bin(int b) { return b >= BIN_MSAD0 && b < BIN_MSAD0 + 3; }
 __host__ __device__ constexpr bool is_msa_bin(int b) { return b >= BIN_MSA0 && b < BIN_MSA0 + 4; }
@@ -123,7 +125,10 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     if (flops == 0 || (!ap.comp && nm == 0)) return BIN_EMPTY;
     const int kind = ap.pair ? 0 : (ap.ordered ? 2 : 1);
     const int tf = flops <= ap.tier_flops0 ? 0 : (flops <= ap.tier_flops1 ? 1 : 2);
-    const int tr = ap.ordered ? 0 : tf;        // ordered float64 runs one warp per row
+    // budget tier of the single-warp-only kernels (dense / sparse MSA) for
+    // ordered float64; the rank and hash families split heavy ordered rows
+    // over a group by output column (ordered_products_f64)
+    const int tr = ap.ordered ? 0 : tf;
     int fam = ap.family;
     // one A entry, many products, a wide mask window: the bitmap filter (cfg4 shape)
     if (fam == FAM_AUTO && na == 1 && words >= 256 && 4 * words <= 98304) return BIN_SINGLE;
@@ -137,7 +142,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             if (ap.has_bt && pull < push) fam = FAM_PULL;
             // ordered float64 rows (one warp, k order): the rank search beats
             // both the bitmap and the hash for short mask rows
-            else if (ap.ordered && nm <= 512) fam = FAM_MCA;
+            else if (ap.ordered && nm <= 512 && msad_bytes(words, kind) > ap.rank_budget[tf]) fam = FAM_MCA;
             // push: the bitmap accumulator when the mask window is compact
             else if (msa_bytes(words, nm, kind) <= ap.rank_budget[tr]) fam = FAM_MSA;
             else if (tr == 0 && nm <= ap.auto_mca_nm) fam = FAM_MCA;
@@ -153,7 +158,8 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         }
         if (na <= 32) return BIN_HEAP0 + 2;
     }
-    if (!ap.comp && fam == FAM_MSA && msa_bytes(words, nm, kind) > ap.rank_budget[tr] &&
+    const bool single_ok = !ap.ordered || tf == 0;
+    if (!ap.comp && fam == FAM_MSA && single_ok && msa_bytes(words, nm, kind) > ap.rank_budget[tr] &&
         msas_bytes(words, nm, kind) <= ap.rank_budget[tr] && nm < 65536) {
         // narrow mask over a wide window: sparse two-level bitmap
         *cap_lg_out = (int)msas_blocks(words, nm);   // per-bin maximum of touched blocks
@@ -161,10 +167,17 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         return BIN_MSAS0 + tr;
     }
     // the dense window when it fits: one load and one compare per product
-    if (!ap.comp && fam == FAM_MSA && msad_bytes(words, kind) <= ap.rank_budget[tr]) return BIN_MSAD0 + tr;
+    if (!ap.comp && fam == FAM_MSA && msad_bytes(words, kind) <= ap.rank_budget[ap.ordered ? tf : tr])
+        return BIN_MSAD0 + (ap.ordered ? tf : tr);
+    // complemented MSA / auto with an output narrow enough for a state per column
+    if (ap.comp && (ap.family == FAM_MSA || ap.family == FAM_AUTO) &&
+        msad_bytes((ncols + 31) >> 5, kind) - (kind == 0 ? 4 : 12) <= ap.rank_budget[tf]) {   // guard column free
+        *aux_out = (ncols + 31) >> 5;
+        return BIN_MSADC0 + tf;
+    }
     if (!ap.comp && (fam == FAM_MSA || fam == FAM_MCA)) {
         const int64_t bytes = fam == FAM_MSA ? msa_bytes(words, nm, kind) : mca_bytes(nm, kind);
-        const int tier = bytes <= ap.rank_budget[tr] ? tr : 3;
+        const int tier = bytes <= ap.rank_budget[tf] ? tf : 3;
         return (fam == FAM_MSA ? BIN_MSA0 : BIN_MCA0) + tier;
     }
     // hash family (and the complement forms of MSA / heap)
@@ -189,9 +202,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     int need = ceil_log2_i64(2 * keys);
     if (need < 5) need = 5;
     int tier;
-    if (ap.ordered) {
-        tier = need <= tier_cap_lg_val(0) ? 0 : 3;
-    } else {
+    {
         int tc = 3;
         for (int t = 0; t < 3; t++) {
             if (need <= tier_cap_lg(ap.pair, t)) { tc = t; break; }
@@ -212,10 +223,18 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     return hash_bin(mode, tier, used > ap.capc_lg ? 1 : 0);
 }
 
+// Rows with more A entries than this (or, when the cost model needs B^T
+// column lengths, more mask entries) are analysed by k_analyze_long, a block
+// per row: hub rows (cfg5: 163,558 entries) would otherwise hold one warp for
+// milliseconds while the rest of the grid idles.
+constexpr int64_t LONG_ROW = 2048;
+
 // One warp per row.  Computes row_flops, 1P complement bounds, bin + table size.
+// Long rows are appended to long_rows[] (count in long_rows_n) instead.
 __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64_t* row_flops,
                                                  int64_t* bound, uint8_t* row_bin, int8_t* row_cap_lg,
-                                                 Summary* s, int64_t* row_nnz) {
+                                                 Summary* s, int64_t* row_nnz, int32_t* long_rows,
+                                                 int* long_rows_n) {
     __shared__ int s_count[NBINS];
     __shared__ int s_cap[NBINS];
     __shared__ unsigned long long s_bflops[NBINS];
@@ -236,13 +255,18 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
     unsigned long long my_flops = 0, my_bound = 0;
     for (int64_t r0 = warp * 32; r0 < p.nrows; r0 += nwarps * 32) {
         const int64_t i = r0 + lane;
-        const bool live = i < p.nrows;
+        bool live = i < p.nrows;
         int64_t as = 0, ae = 0, ms = 0, me = 0;
         if (live) {
             as = p.a_ptr[i];
             ae = p.a_ptr[i + 1];
             ms = p.m_ptr[i];
             me = p.m_ptr[i + 1];
+            if (ae - as > LONG_ROW || (want_pull && me - ms > LONG_ROW)) {
+                long_rows[atomicAdd(long_rows_n, 1)] = (int32_t)i;
+                live = false;
+                as = ae = ms = me = 0;
+            }
         }
         long long f = 0;
         if (ae - as <= 32) {
@@ -363,6 +387,81 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
         atomicMax(&s->max_nm, s_nm);
     }
 }
+
+// Long rows (see LONG_ROW): one block per row, same quantities and the same
+// classification as k_analyze, folded into the summary with global atomics.
+// Runs after k_analyze on the same stream; grid-strides over the list.
+__global__ void __launch_bounds__(256) k_analyze_long(Prob p, AnalyzeParams ap, int64_t* row_flops,
+                                                      int64_t* bound, uint8_t* row_bin, int8_t* row_cap_lg,
+                                                      Summary* s, int64_t* row_nnz, const int32_t* long_rows,
+                                                      const int* long_rows_n) {
+    __shared__ long long s_red[8];
+    const int n_long = *long_rows_n;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool want_pull = ap.family == FAM_AUTO && ap.has_bt && !ap.comp;
+    for (int q = blockIdx.x; q < n_long; q += gridDim.x) {
+        const int64_t i = long_rows[q];
+        const int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1], ms = p.m_ptr[i], me = p.m_ptr[i + 1];
+        long long f = 0;
+        int64_t t = as + threadIdx.x;
+        for (; t + 3 * 256 < ae; t += 4 * 256) {
+            const int32_t k0 = p.a_idx[t], k1 = p.a_idx[t + 256], k2 = p.a_idx[t + 512], k3 = p.a_idx[t + 768];
+            f += (p.b_ptr[k0 + 1] - p.b_ptr[k0]) + (p.b_ptr[k1 + 1] - p.b_ptr[k1]) +
+                 (p.b_ptr[k2 + 1] - p.b_ptr[k2]) + (p.b_ptr[k3 + 1] - p.b_ptr[k3]);
+        }
+        for (; t < ae; t += 256) {
+            const int32_t k = p.a_idx[t];
+            f += p.b_ptr[k + 1] - p.b_ptr[k];
+        }
+        f = warp_sum_ll(f);
+        if (lane == 0) s_red[wid] = f;
+        __syncthreads();
+        f = 0;
+        for (int w = 0; w < 8; w++) f += s_red[w];
+        __syncthreads();
+        const int64_t nm = me - ms;
+        long long pull_cols = 0;
+        if (want_pull && f > 0 && nm > 0) {
+            for (int64_t u = ms + threadIdx.x; u < me; u += 256) {
+                const int32_t j = p.m_idx[u];
+                pull_cols += p.bt_ptr[j + 1] - p.bt_ptr[j];
+            }
+            pull_cols = warp_sum_ll(pull_cols);
+            if (lane == 0) s_red[wid] = pull_cols;
+            __syncthreads();
+            pull_cols = 0;
+            for (int w = 0; w < 8; w++) pull_cols += s_red[w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const int64_t na = ae - as;
+            row_flops[i] = f;
+            unsigned long long bd = 0;
+            if (bound) {
+                bd = f < p.ncols ? f : p.ncols;
+                bound[i] = bd;
+            }
+            int64_t words = nm > 0 ? (((int64_t)p.m_idx[me - 1] - p.m_idx[ms]) >> 5) + 1 : 0;
+            int cap_lg = 0;
+            const int b = classify_row(ap, na, nm, f, p.ncols, pull_cols, words, &cap_lg, &words);
+            row_bin[i] = (uint8_t)b;
+            row_cap_lg[i] = (int8_t)cap_lg;
+            if (row_nnz && b == BIN_EMPTY) row_nnz[i] = 0;
+            atomicAdd(&s->bin_count[b], 1);
+            atomicAdd(&s->bin_flops[b], (unsigned long long)f);
+            if (cap_lg) atomicMax(&s->bin_cap_lg[b], cap_lg);
+            if (b != BIN_EMPTY) {
+                atomicMax(&s->bin_words[b], (int)(words < 0x7fffffff ? words : 0x7fffffff));
+                atomicMax(&s->bin_nmmax[b], (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
+            }
+            atomicAdd(&s->gen_flops, (unsigned long long)f);
+            atomicAdd(&s->bound_total, bd);
+            atomicMax(&s->max_na, (int)(na < 0x7fffffff ? na : 0x7fffffff));
+            atomicMax(&s->max_nm, (int)(nm < 0x7fffffff ? nm : 0x7fffffff));
+        }
+    }
+}
+
 
 // Scatter row ids into per-bin lists (warp-aggregated atomics).
 // Bin offsets come from the analysis summary (same rule as the host:

@@ -111,6 +111,17 @@ __device__ __forceinline__ int owner_of(int incl, int q) {
     return l;
 }
 
+// first position in idx[lo, hi) whose value is >= key
+__device__ __forceinline__ int64_t lower_bound_range(const int32_t* __restrict__ idx, int64_t lo, int64_t hi,
+                                                     int32_t key) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (idx[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 // lower_bound over a sorted int32 array.
 __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* a, int64_t n, int32_t key) {
     int64_t lo = 0, hi = n;

@@ -16,17 +16,6 @@
 
 namespace mm {
 
-// first position in idx[lo, hi) whose value is >= key
-__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ idx, int64_t lo, int64_t hi,
-                                                   int32_t key) {
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (idx[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
 enum LookupOp : int { LK_VALUE = 0, LK_BC_WEIGHT = 1, LK_SCALE = 2 };
 
 // Per X entry t (row i, column j):
@@ -49,7 +38,7 @@ __global__ void __launch_bounds__(256) k_lookup(int64_t nrows, const int64_t* __
         const int64_t ys = y_ptr[i], ye = y_ptr[i + 1];
         for (int64_t t = xs + lane; t < xe; t += 32) {
             const int32_t j = x_idx[t];
-            const int64_t p = lower_bound_i32(y_idx, ys, ye, j);
+            const int64_t p = lower_bound_range(y_idx, ys, ye, j);
             const bool hit = p < ye && y_idx[p] == j;
             const T y = hit ? y_val[p] : T(0);
             if (OP == LK_VALUE) {
@@ -57,7 +46,7 @@ __global__ void __launch_bounds__(256) k_lookup(int64_t nrows, const int64_t* __
                 if (found) found[t] = hit;
             } else if (OP == LK_BC_WEIGHT) {
                 const int64_t zs = z_ptr[i], ze = z_ptr[i + 1];
-                const int64_t q = lower_bound_i32(z_idx, zs, ze, j);
+                const int64_t q = lower_bound_range(z_idx, zs, ze, j);
                 const T z = (q < ze && z_idx[q] == j) ? z_val[q] : T(0);
                 out[t] = (T(1) + y) / z;
             } else {
@@ -81,7 +70,7 @@ __global__ void __launch_bounds__(256) k_ewise_count(int64_t nrows, const int64_
         if (as < ae && bs < be)
             for (int64_t t = as + lane; t < ae; t += 32) {
                 const int32_t j = a_idx[t];
-                const int64_t p = lower_bound_i32(b_idx, bs, be, j);
+                const int64_t p = lower_bound_range(b_idx, bs, be, j);
                 both += p < be && b_idx[p] == j;
             }
         both = __reduce_add_sync(FULL, both);
@@ -116,7 +105,7 @@ __global__ void __launch_bounds__(256) k_ewise_fill(int64_t nrows, const int64_t
             bool hit = false;
             if (live) {
                 j = a_idx[t];
-                p = lower_bound_i32(b_idx, bs, be, j);
+                p = lower_bound_range(b_idx, bs, be, j);
                 hit = p < be && b_idx[p] == j;
             }
             const unsigned hits = __ballot_sync(FULL, hit);
@@ -136,7 +125,7 @@ __global__ void __launch_bounds__(256) k_ewise_fill(int64_t nrows, const int64_t
             bool hit = false;
             if (live) {
                 j = b_idx[s];
-                p = lower_bound_i32(a_idx, as, ae, j);
+                p = lower_bound_range(a_idx, as, ae, j);
                 hit = p < ae && a_idx[p] == j;
             }
             const unsigned hits = __ballot_sync(FULL, hit);
@@ -167,7 +156,7 @@ __global__ void __launch_bounds__(256) k_bc_accumulate(int64_t nrows, const int6
         double acc = scores[r];
         for (int64_t t = s; t < e; t++) acc += d_val[t];
         if (own >= 0) {
-            const int64_t p = lower_bound_i32(d_idx, s, e, own);
+            const int64_t p = lower_bound_range(d_idx, s, e, own);
             acc -= (p < e && d_idx[p] == own) ? d_val[p] : 0.0;
         }
         scores[r] = acc;

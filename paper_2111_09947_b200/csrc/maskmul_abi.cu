@@ -263,8 +263,11 @@ HashKernel pick_hash_unordered(int tier, int* gw) {
 
 template <int MODE>
 HashKernel pick_hash_ordered(int tier, int* gw) {
-    *gw = 1;
-    return tier == 0 ? k_push_hash<1, true, 2, MODE, true> : k_push_hash<1, false, 2, MODE, true>;
+    // shared tiers: groups split ordered rows by column; the global tier
+    // keeps one warp per row (its rows are there for their table size, not
+    // their work)
+    if (tier == 3) { *gw = 1; return k_push_hash<1, false, 2, MODE, true>; }
+    return pick_hash_unordered<2, MODE, true>(tier, gw);
 }
 
 template <int MODE>
@@ -279,6 +282,23 @@ HashKernel pick_hash(int kind, int mode, int tier, bool numeric, int* gw) {
     if (mode == MODE_PLAIN) return pick_hash_mode<MODE_PLAIN>(kind, tier, numeric, gw);
     if (mode == MODE_CTAB) return pick_hash_mode<MODE_CTAB>(kind, tier, numeric, gw);
     return pick_hash_mode<MODE_CSRCH>(kind, tier, numeric, gw);
+}
+
+typedef void (*DenseKernel)(Prob, Out, Work, int);
+
+template <bool COMP, int GW>
+DenseKernel pick_dense_gw(int kind, bool numeric) {
+    if (!numeric) return k_push_dense<GW, 0, false, COMP>;
+    if (kind == 0) return k_push_dense<GW, 0, true, COMP>;
+    if (kind == 1) return k_push_dense<GW, 1, true, COMP>;
+    return k_push_dense<GW, 2, true, COMP>;
+}
+
+template <bool COMP>
+DenseKernel pick_dense(int kind, bool numeric, int gw) {
+    if (gw == 1) return pick_dense_gw<COMP, 1>(kind, numeric);
+    if (gw == 4) return pick_dense_gw<COMP, 4>(kind, numeric);
+    return pick_dense_gw<COMP, 8>(kind, numeric);
 }
 
 typedef void (*RankKernel)(Prob, Out, Work, int, int, unsigned char*);
@@ -304,8 +324,10 @@ RankKernel pick_rank(int kind, int tier, bool numeric, int* gw) {
     if (!numeric || kind == 0) return numeric ? pick_rank_unordered<0, MSA, true>(tier, gw)
                                               : pick_rank_unordered<0, MSA, false>(tier, gw);
     if (kind == 1) return pick_rank_unordered<1, MSA, true>(tier, gw);
-    *gw = 1;
-    return tier == 0 ? k_push_rank<1, true, 2, MSA, true> : k_push_rank<1, false, 2, MSA, true>;
+    // ordered float64: groups split rows by column in the shared tiers, one
+    // warp per row in the global tier (see pick_hash_ordered)
+    if (tier == 3) { *gw = 1; return k_push_rank<1, false, 2, MSA, true>; }
+    return pick_rank_unordered<2, MSA, true>(tier, gw);
 }
 
 // Launch every non-empty bin.  numeric=false: symbolic counts into out.row_nnz.
@@ -368,7 +390,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             int kind = numeric ? h->kind : 0;
             int gw = 1;
             HashKernel kern = pick_hash(kind, mode, tier, numeric, &gw);
-            bool smem_table = kind == 2 ? tier == 0 : tier < 3;
+            bool smem_table = tier < 3;
             int threads = gw == 32 ? 1024 : (gw == 16 ? 512 : 256);
             int groups = threads / (32 * gw);
             int cap_lg = std::max(h->sum.bin_cap_lg[b], 5);
@@ -463,20 +485,14 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             CU(cudaGetLastError());
             continue;
         }
-        if (is_msad_bin(b)) {
-            const int tier = b - BIN_MSAD0;
+        if (is_msad_bin(b) || is_msadc_bin(b)) {
+            const bool comp = is_msadc_bin(b);
+            const int tier = b - (comp ? BIN_MSADC0 : BIN_MSAD0);
             const int kind = numeric ? h->kind : 0;
             void (*kern)(Prob, Out, Work, int) = nullptr;
-            const int gw = kind == 2 ? 1 : (tier == 0 ? 1 : (tier == 1 ? MM_RANK_T1_GW : MM_RANK_T2_GW));
-            if (kind == 2) {
-                kern = k_push_dense<1, 2, true>;
-            } else if (!numeric || kind == 0) {
-                if (gw == 1) kern = numeric ? k_push_dense<1, 0, true> : k_push_dense<1, 0, false>;
-                else if (gw == 4) kern = numeric ? k_push_dense<4, 0, true> : k_push_dense<4, 0, false>;
-                else kern = numeric ? k_push_dense<8, 0, true> : k_push_dense<8, 0, false>;
-            } else {
-                kern = gw == 1 ? k_push_dense<1, 1, true> : (gw == 4 ? k_push_dense<4, 1, true> : k_push_dense<8, 1, true>);
-            }
+            const int gw = tier == 0 ? 1 : (tier == 1 ? MM_RANK_T1_GW : MM_RANK_T2_GW);
+            if (comp) kern = pick_dense<true>(kind, numeric, gw);
+            else kern = pick_dense<false>(kind, numeric, gw);
             const int groups = 256 / (32 * gw);
             const int words_max = std::max(h->sum.bin_words[b], 1);
             const size_t rb = (dense_region_bytes(kind, words_max) + 15) & ~(size_t)15;
@@ -628,7 +644,9 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     const int64_t scan_elems = scan_scratch_elems(m);
     size_t off = 0;
     auto carve = [&](size_t bytes) { size_t at = off; off += (bytes + 255) & ~(size_t)255; return at; };
-    const size_t o_sum = carve(sizeof(Summary) + 3 * NBINS * sizeof(int32_t));
+    const size_t zero_bytes = sizeof(Summary) + (3 * NBINS + 4) * sizeof(int32_t);   // + long-row count
+    const size_t o_sum = carve(zero_bytes);
+    const size_t o_long = carve(m * sizeof(int32_t));
     const size_t o_flops = carve(m * sizeof(int64_t));
     const size_t o_nnz = carve(m * sizeof(int64_t));
     const size_t o_ptr = carve((m + 1) * sizeof(int64_t));
@@ -644,6 +662,8 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     if ((rc = dalloc(h, &slab, off))) return rc;
     h->d_summary = (Summary*)(slab + o_sum);
     h->cursors = (int32_t*)(slab + o_sum + sizeof(Summary));
+    int* long_n = (int*)(h->cursors + 3 * NBINS);
+    int32_t* long_rows = (int32_t*)(slab + o_long);
     h->row_flops = (int64_t*)(slab + o_flops);
     h->row_nnz = (int64_t*)(slab + o_nnz);
     h->c_row_ptr = (int64_t*)(slab + o_ptr);
@@ -656,14 +676,22 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     h->tmp_idx = plain_1p ? (int32_t*)(slab + o_tidx) : nullptr;
     h->tmp_val = plain_1p ? (void*)(slab + o_tval) : nullptr;
     p.row_flops = h->row_flops;
-    CU(cudaMemsetAsync(h->d_summary, 0, sizeof(Summary) + 3 * NBINS * sizeof(int32_t), st));
+    CU(cudaMemsetAsync(h->d_summary, 0, zero_bytes, st));
 
     if (m > 0) {
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
+        int64_t* zero_nnz = symbolic_only ? nullptr : h->row_nnz;
         ++g_launches;
         k_analyze<<<grid, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin, h->row_cap_lg,
-                                        h->d_summary, symbolic_only ? nullptr : h->row_nnz);
+                                        h->d_summary, zero_nnz, long_rows, long_n);
         CU(cudaGetLastError());
+        if (a->nnz > LONG_ROW || (ap.has_bt && mask->nnz > LONG_ROW)) {   // a long row is possible
+            ++g_launches;
+            k_analyze_long<<<h->num_sms * 2, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin,
+                                                            h->row_cap_lg, h->d_summary, zero_nnz, long_rows,
+                                                            long_n);
+            CU(cudaGetLastError());
+        }
     }
     if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
     h->sum = *h->h_summary;
@@ -937,19 +965,25 @@ int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops,
     Summary* s = nullptr;
     uint8_t* rb = nullptr;
     int8_t* rc_lg = nullptr;
-    CU(cudaMallocAsync((void**)&s, sizeof(Summary), st));
+    int32_t* long_rows = nullptr;
+    CU(cudaMallocAsync((void**)&s, sizeof(Summary) + 16, st));
+    CU(cudaMallocAsync((void**)&long_rows, std::max<int64_t>(a->nrows, 1) * sizeof(int32_t), st));
+    int* long_n = (int*)(s + 1);
     CU(cudaMallocAsync((void**)&rb, std::max<int64_t>(a->nrows, 1), st));
     CU(cudaMallocAsync((void**)&rc_lg, std::max<int64_t>(a->nrows, 1), st));
-    CU(cudaMemsetAsync(s, 0, sizeof(Summary), st));
+    CU(cudaMemsetAsync(s, 0, sizeof(Summary) + 16, st));
     if (a->nrows > 0) {
         int grid = (int)std::min<int64_t>((a->nrows + 255) / 256, 148 * 8);
         ++g_launches;
-        k_analyze<<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr);
+        k_analyze<<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr, long_rows, long_n);
+        ++g_launches;
+        k_analyze_long<<<296, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr, long_rows, long_n);
     }
     if (total) CU(cudaMemcpyAsync(total, &s->gen_flops, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     cudaFreeAsync(s, st);
     cudaFreeAsync(rb, st);
     cudaFreeAsync(rc_lg, st);
+    cudaFreeAsync(long_rows, st);
     CU(cudaGetLastError());
     return MM_OK;
 }

@@ -305,9 +305,17 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
 // slot (two k's hitting one column) fold one after another in lane order
 // (__match_any_sync ranks them), everyone else folds at once.
 // loc.locate(j) -> slot or -1 (masked out); loc.fold(slot, prod); loc.mark(slot).
+//
+// Groups of several warps split a heavy row by OUTPUT COLUMN: a warp takes
+// only the products with column in [c_lo, c_hi) (each B row is sorted, so
+// its share of B_k is a sub-range found by two binary searches).  Every slot
+// then belongs to exactly one warp, which still folds it in ascending k: the
+// parallelism is across slots, the order inside a slot is untouched.
 template <bool NUMERIC, class LOC>
 __device__ __forceinline__ unsigned ordered_products_f64(const Prob& p, LOC& loc, int64_t as, int64_t ae,
-                                                         int lane) {
+                                                         int lane, int32_t c_lo = INT32_MIN,
+                                                         int32_t c_hi = INT32_MAX) {
+    const bool split = c_lo != INT32_MIN || c_hi != INT32_MAX;
     const double* av_p = (const double*)p.a_val;
     const double* bv_p = (const double*)p.b_val;
     unsigned evaluated = 0;
@@ -319,7 +327,12 @@ __device__ __forceinline__ unsigned ordered_products_f64(const Prob& p, LOC& loc
         if (t < ae) {
             const int32_t k = p.a_idx[t];
             bs = p.b_ptr[k];
-            len = (int)(p.b_ptr[k + 1] - bs);
+            int64_t be = p.b_ptr[k + 1];
+            if (split) {
+                if (c_lo != INT32_MIN) bs = lower_bound_range(p.b_idx, bs, be, c_lo);
+                if (c_hi != INT32_MAX) be = lower_bound_range(p.b_idx, bs, be, c_hi);
+            }
+            len = (int)(be - bs);
             av = av_p[t];
         }
         const int incl = warp_incl_scan(len, lane);

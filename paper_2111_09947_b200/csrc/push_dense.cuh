@@ -16,6 +16,13 @@
 // products that survive the mask, one shared atomic.  Chosen (msa / auto)
 // when the window fits the tier's budget; otherwise the rank-compressed MSA
 // of push_rank.cuh.
+//
+// COMP: the complemented-mask MSA (_kernels.py:36-40,66-77) for outputs
+// narrow enough that every column fits (ncols columns, e.g. the 512 source
+// columns of a betweenness-centrality batch): the array is ALLOWED (0) between
+// rows, a row marks its mask columns DENIED, products land on any other
+// column, and the gather walks the columns in order (the reference sorts the
+// inserted keys, :69) before restoring the array.
 #pragma once
 #include "common.cuh"
 #include "product_loop.cuh"
@@ -88,30 +95,109 @@ struct DenseWindow {
     }
 };
 
+// Complement gather: warp w owns columns [w ncols/GW, (w+1) ncols/GW); set
+// columns are emitted in column order and reset to ALLOWED, then the row's
+// mask columns are restored to ALLOWED.
 template <int GW, int KIND, bool NUMERIC>
+__device__ __forceinline__ void dense_gather_comp(const Prob& p, const Out& o, int32_t* cnt, unsigned long long* val,
+                                                  const RowInfo& ri, int gt, int bar_id, int* s_warp, int64_t w0,
+                                                  unsigned long long& evaluated) {
+    constexpr int GT = GW * 32;
+    const int lane = gt & 31, wg = gt >> 5;
+    const int c_lo = (int)(p.ncols * wg / GW), c_hi = (int)(p.ncols * (wg + 1) / GW);
+    int mine = 0;
+    for (int c = c_lo + lane; c < c_hi; c += 32) {
+        const int v = cnt[c];
+        mine += v > 0;
+        if (KIND == 0 && NUMERIC && v > 0) evaluated += (unsigned)v;
+    }
+    mine = (int)warp_sum_ll(mine);
+    int before = 0, total = mine;
+    if (GW > 1) {
+        if (lane == 0) s_warp[wg] = mine;
+        group_bar(bar_id, GT);
+        total = 0;
+#pragma unroll
+        for (int q = 0; q < GW; q++) {
+            const int c = s_warp[q];
+            if (q < wg) before += c;
+            total += c;
+        }
+    }
+    int run = before;
+    for (int cb = c_lo; cb < c_hi; cb += 32) {
+        const int c = cb + lane;
+        const int v = c < c_hi ? cnt[c] : 0;
+        const bool set = v > 0;
+        const unsigned bal = __ballot_sync(FULL, set);
+        if (set) {
+            if (NUMERIC) {
+                const int64_t d = w0 + run + __popc(bal & lanemask_lt());
+                o.idx[d] = c;
+                if (KIND == 0) {
+                    if (o.out_f64) ((double*)o.val)[d] = (double)v;
+                    else ((long long*)o.val)[d] = v;
+                } else {
+                    ((unsigned long long*)o.val)[d] = val[c];
+                }
+            }
+            cnt[c] = 0;
+            if (KIND != 0) val[c] = 0ull;
+        }
+        run += __popc(bal);
+    }
+    if (gt == 0) o.row_nnz[ri.i] = total;
+    group_bar(bar_id, GT);
+    for (int64_t t = ri.ms + gt; t < ri.me; t += GT) cnt[p.m_idx[t]] = 0;
+    group_bar(bar_id, GT);
+}
+
+template <int GW, int KIND, bool NUMERIC, bool COMP>
 __device__ __forceinline__ void dense_row(const Prob& p, const Out& o, int32_t* cnt, unsigned long long* val,
                                           int words_max, const RowInfo& ri, int gt, int bar_id, int* s_warp,
                                           BatchSmem bsm, unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
     const int lane = gt & 31;
+    const int wg = gt >> 5;
     const int64_t i = ri.i, as = ri.as, ae = ri.ae, ms = ri.ms, me = ri.me;
     const int nm = (int)(me - ms);
-    const int32_t lo = p.m_idx[ms];
-    const int32_t hi = p.m_idx[me - 1];
+    const int32_t lo = COMP ? 0 : p.m_idx[ms];
+    const int32_t hi = COMP ? (int32_t)(p.ncols - 1) : p.m_idx[me - 1];
 
-    // 1. mark the mask columns (the window is DENIED everywhere else)
+    // 1. mark the mask columns (plain: the window is DENIED everywhere else;
+    //    complement: ALLOWED everywhere else)
     for (int r = gt; r < nm; r += GT) {
         const int32_t off = p.m_idx[ms + r] - lo;
-        cnt[off] = 0;
-        if (KIND != 0) val[off] = 0ull;
+        if (COMP) {
+            cnt[off] = DENIED;
+        } else {
+            cnt[off] = 0;
+            if (KIND != 0) val[off] = 0ull;
+        }
     }
     group_bar(bar_id, GT);
 
     // 2. products
     if (KIND == 2) {
+        // groups split the row by output column (see ordered_products_f64):
+        // plain by mask rank (the ranks warp wg gathers), complement by column
+        int32_t c_lo = INT32_MIN, c_hi = INT32_MAX;
+        bool idle = false;
+        if (GW > 1) {
+            if (COMP) {
+                c_lo = wg == 0 ? INT32_MIN : (int32_t)(p.ncols * wg / GW);
+                c_hi = wg == GW - 1 ? INT32_MAX : (int32_t)(p.ncols * (wg + 1) / GW);
+                idle = wg > 0 && wg < GW - 1 && c_lo == c_hi;
+            } else {
+                const int r0 = (int)(((long long)nm * wg) / GW), r1 = (int)(((long long)nm * (wg + 1)) / GW);
+                idle = r0 == r1;
+                c_lo = wg == 0 ? INT32_MIN : p.m_idx[ms + r0];
+                c_hi = r1 < nm ? p.m_idx[ms + r1] : INT32_MAX;
+            }
+        }
         DenseWindow win{cnt, lo, (uint32_t)(hi - lo)};
         RankLocatorF64<DenseWindow> loc{win, cnt, (double*)val};
-        evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+        if (!idle) evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane, c_lo, c_hi);
     } else {
         DenseProber<KIND, NUMERIC> pr;
         pr.cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
@@ -126,9 +212,12 @@ __device__ __forceinline__ void dense_row(const Prob& p, const Out& o, int32_t* 
     group_bar(bar_id, GT);
 
     // 3. gather in mask order (warp w owns mask entries [w nm/GW, (w+1) nm/GW)),
-    //    restoring DENIED behind it
+    //    restoring DENIED behind it; complement: in column order
     const int64_t w0 = NUMERIC ? o.off[i] : 0;
-    const int wg = gt >> 5;
+    if (COMP) {
+        dense_gather_comp<GW, KIND, NUMERIC>(p, o, cnt, val, ri, gt, bar_id, s_warp, w0, evaluated);
+        return;
+    }
     const int r_lo = (int)(((long long)nm * wg) / GW), r_hi = (int)(((long long)nm * (wg + 1)) / GW);
     int mine = 0;
     for (int r = r_lo + lane; r < r_hi; r += 32) {
@@ -180,7 +269,7 @@ __device__ __forceinline__ void dense_row(const Prob& p, const Out& o, int32_t* 
 #ifndef MM_DENSE_MINB
 #define MM_DENSE_MINB 5
 #endif
-template <int GW, int KIND, bool NUMERIC>
+template <int GW, int KIND, bool NUMERIC, bool COMP = false>
 __global__ void __launch_bounds__(256, GW <= 8 ? MM_DENSE_MINB : 1)
 k_push_dense(Prob p, Out o, Work wk, int words_max) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -198,13 +287,18 @@ k_push_dense(Prob p, Out o, Work wk, int words_max) {
     int32_t* cnt = (int32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)ncol));
     unsigned char* bbase = smem + (size_t)groups * rbytes + (size_t)g * batch_bytes<GW, KIND>();
     BatchSmem bsm = bind_batch<GW, KIND>(bbase);
-    for (int c = gt; c < ncol; c += GT) cnt[c] = DENIED;
+    for (int c = gt; c < ncol; c += GT) {
+        // complement: ALLOWED columns with zero values, the guard DENIED
+        cnt[c] = COMP && c < ncol - 1 ? 0 : DENIED;
+        if (COMP && KIND != 0) val[c] = 0ull;
+    }
     group_bar(bar_id, GT);
     unsigned long long evaluated = 0;
     RowFetcher<GW> rf;
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
-        dense_row<GW, KIND, NUMERIC>(p, o, cnt, val, words_max, ri, gt, bar_id, s_warp + g * GW, bsm, evaluated);
+        dense_row<GW, KIND, NUMERIC, COMP>(p, o, cnt, val, words_max, ri, gt, bar_id, s_warp + g * GW, bsm,
+                                           evaluated);
     if (NUMERIC) {
         const long long e = warp_sum_ll((long long)evaluated);
         if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);

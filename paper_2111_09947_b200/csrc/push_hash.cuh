@@ -529,8 +529,24 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
 
     // 3. products
     if (KIND == 2) {
+        // ordered float64 in a group: warp wg folds its own output columns —
+        // a slice of the mask row (plain) or of [0, ncols) (complement)
+        int32_t c_lo = INT32_MIN, c_hi = INT32_MAX;
+        bool idle = false;
+        if (GW > 1) {
+            if (MODE == MODE_PLAIN) {
+                const int64_t r0 = nm * wg / GW, r1 = nm * (wg + 1) / GW;
+                idle = r0 == r1;
+                c_lo = wg == 0 ? INT32_MIN : p.m_idx[ms + r0];
+                c_hi = r1 < nm ? p.m_idx[ms + r1] : INT32_MAX;
+            } else {
+                c_lo = wg == 0 ? INT32_MIN : (int32_t)(p.ncols * wg / GW);
+                c_hi = wg == GW - 1 ? INT32_MAX : (int32_t)(p.ncols * (wg + 1) / GW);
+                idle = c_lo != INT32_MIN && c_hi != INT32_MAX && c_lo == c_hi;
+            }
+        }
         HashLocatorF64<MODE> loc{tb.keys, tb.cnt, (double*)tb.val, cap_lg, cmask, p.m_idx + ms, me - ms};
-        evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+        if (!idle) evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane, c_lo, c_hi);
     } else if (CLEAN && pl.hm == 1) {
         DirectProber<KIND, NUMERIC, 1> pr;
         pr.keys_s = (uint32_t)__cvta_generic_to_shared(tb.keys);

@@ -271,16 +271,28 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     group_bar(bar_id, GT);
 
     // 3. products
+    // ordered float64 in a group: warp wg folds the columns of mask ranks
+    // [wg nm/GW, (wg+1) nm/GW) — the same ranks it gathers in step 4
+    int32_t c_lo = INT32_MIN, c_hi = INT32_MAX;
+    bool idle = false;
+    if (KIND == 2 && GW > 1) {
+        const int wg = gt >> 5;
+        const int r0 = (int)(((long long)nm * wg) / GW), r1 = (int)(((long long)nm * (wg + 1)) / GW);
+        idle = r0 == r1;
+        c_lo = wg == 0 ? INT32_MIN : p.m_idx[ms + r0];
+        c_hi = r1 < nm ? p.m_idx[ms + r1] : INT32_MAX;
+    }
     if (MSA) {
         if (KIND == 2) {
-            if (SMEM) {
+            if (idle) {
+            } else if (SMEM) {
                 MsaPacked rb{bits, lo, (uint32_t)(hi - lo)};
                 RankLocatorF64<MsaPacked> loc{rb, sl.cnt, (double*)sl.val};
-                evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+                evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane, c_lo, c_hi);
             } else {
                 MsaBits<int32_t> rb{bits, pre, lo, (uint32_t)(hi - lo)};
                 RankLocatorF64<MsaBits<int32_t>> loc{rb, sl.cnt, (double*)sl.val};
-                evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+                evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane, c_lo, c_hi);
             }
         } else {
           if (!SMEM) {
@@ -307,7 +319,7 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
         McaRow rb{mrow, nm, steps};
         if (KIND == 2) {
             RankLocatorF64<McaRow> loc{rb, sl.cnt, (double*)sl.val};
-            evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane);
+            if (!idle) evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane, c_lo, c_hi);
         } else {
             RankProber<KIND, NUMERIC, McaRow> pr{rb, sl, p.b_val, 0u};
             flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
