@@ -217,7 +217,10 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     const int ls = tier == 2 && mode == MODE_PLAIN ? ap.load_shift_wide : ap.load_shift;
     int want = ceil_log2_i64(keys << ls);
     if (want < 5) want = 5;
-    int lim = tier_cap_lg(ap.pair, tier);
+    // plain rows past the shared tiers: sliced over the largest shared table
+    // (hash_row), not a global table
+    const bool sliced = tier == 3 && mode == MODE_PLAIN && !ap.ordered;
+    int lim = tier_cap_lg(ap.pair, sliced ? 2 : tier);
     const int used = want < lim ? want : lim;
     *cap_lg_out = used;
     return hash_bin(mode, tier, used > ap.capc_lg ? 1 : 0);

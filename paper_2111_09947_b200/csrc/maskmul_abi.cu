@@ -389,14 +389,18 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             int mode = hash_bin_mode(b), tier = hash_bin_tier(b);
             int kind = numeric ? h->kind : 0;
             int gw = 1;
-            HashKernel kern = pick_hash(kind, mode, tier, numeric, &gw);
-            bool smem_table = tier < 3;
+            // plain tier-3 rows (int64 / plus-pair): sliced over the 16-warp
+            // tier's largest shared table (hash_row), their own launch
+            const bool sliced = tier == 3 && mode == MODE_PLAIN && kind != 2;
+            HashKernel kern = pick_hash(kind, mode, sliced ? 2 : tier, numeric, &gw);
+            bool smem_table = tier < 3 || sliced;
             int threads = gw == 32 ? 1024 : (gw == 16 ? 512 : 256);
             int groups = threads / (32 * gw);
             int cap_lg = std::max(h->sum.bin_cap_lg[b], 5);
             // plain masks in shared memory: room for collision-free direct tables
-            if (mode == MODE_PLAIN && smem_table && kind != 2 && h->direct_lg[tier] > cap_lg)
-                cap_lg = std::min(h->direct_lg[tier], tier_cap_lg(kind == 0, tier));
+            const int ltier = sliced ? 2 : tier;
+            if (mode == MODE_PLAIN && smem_table && kind != 2 && h->direct_lg[ltier] > cap_lg)
+                cap_lg = std::min(h->direct_lg[ltier], tier_cap_lg(kind == 0, ltier));
             size_t ebytes = kind == 0 ? 8 : 16;
             size_t table = ((size_t)1 << cap_lg) * ebytes;
             size_t batch = batch_bytes_rt(gw, kind);

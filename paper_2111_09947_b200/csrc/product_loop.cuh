@@ -177,9 +177,12 @@ __device__ __forceinline__ void tail_chunk(const Prob& p, PR& pr, const int32_t*
 //        lane found by a shuffle binary search.
 //   Every lane calls pr.put(j, a, s) with j = EMPTY_KEY when it has no
 //   product (the policy may use warp collectives).
+//   [c_lo, c_hi): only products with a column in this range (a sub-range of
+//   each sorted B row, by binary search); the default is every product.
 template <int GW, int KIND, class PR>
 __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as, int64_t ae, int gt,
-                                              int bar_id, int* s_warp, BatchSmem bsm) {
+                                              int bar_id, int* s_warp, BatchSmem bsm,
+                                              int32_t c_lo = INT32_MIN, int32_t c_hi = INT32_MAX) {
     constexpr int GT = GW * 32;
 #ifndef MM_PRODUCT_UNROLL
 #define MM_PRODUCT_UNROLL 4
@@ -195,7 +198,10 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
         if (t < ae) {
             const int32_t k = p.a_idx[t];
             base = p.b_ptr[k];
-            len = (int)(p.b_ptr[k + 1] - base);
+            int64_t end = p.b_ptr[k + 1];
+            if (c_lo != INT32_MIN) base = lower_bound_range(p.b_idx, base, end, c_lo);
+            if (c_hi != INT32_MAX) end = lower_bound_range(p.b_idx, base, end, c_hi);
+            len = (int)(end - base);
             if (KIND == 1) av = ((const long long*)p.a_val)[t];
         }
         int tot;

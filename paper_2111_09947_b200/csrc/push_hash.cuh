@@ -421,8 +421,12 @@ struct HashLocatorF64 {
 // ---------------------------------------------------------------------------
 // The row processor.
 // ---------------------------------------------------------------------------
+// One part of a row: the mask entries [ms, me) and the products whose column
+// lies in [c_lo, c_hi) (the whole row unless the row is sliced, see
+// hash_row).  Writes its results at w_base (NUMERIC) and returns their count.
 template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
-__device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
+__device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
+                                         int64_t ms, int64_t me, int32_t c_lo, int32_t c_hi, int64_t w_base,
                                          int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
                                          BatchSmem bsm, unsigned char* wq,
                                          unsigned long long& evaluated) {
@@ -433,7 +437,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     constexpr bool CLEAN = MODE == MODE_PLAIN && SMEM && KIND != 2;
     const int lane = gt & 31;
     const int wg = gt >> 5;
-    const int64_t i = ri.i, as = ri.as, ae = ri.ae, ms = ri.ms, me = ri.me;
+    const int64_t as = ri.as, ae = ri.ae;
     const int64_t nm = me - ms;
     Placement pl{0, cap_lg, FIB_MULT, 0u};
     // group-wide OR of a per-thread flag
@@ -558,7 +562,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         pr.half = 0u;
         pr.b_val = p.b_val;
         pr.evaluated = 0;
-        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
         evaluated += pr.evaluated;
     } else if (CLEAN && pl.hm == 2) {
         DirectProber<KIND, NUMERIC, 2> pr;
@@ -571,7 +575,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         pr.half = 1u << (cap_lg - 1);
         pr.b_val = p.b_val;
         pr.evaluated = 0;
-        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
         evaluated += pr.evaluated;
     } else {
         WarpProber<KIND, MODE, NUMERIC, SMEM> pr;
@@ -589,13 +593,13 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         pr.qn = 0;
         pr.lane = lane;
         pr.evaluated = 0;
-        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
+        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
         evaluated += pr.evaluated;
     }
     group_bar(bar_id, GT);
 
     // 4. gather
-    const int64_t w = NUMERIC ? o.off[i] : 0;
+    const int64_t w = w_base;
     int running = 0;
     if (MODE == MODE_PLAIN) {
         // mask order, like the reference's gather (_kernels.py:78-85,208-216)
@@ -688,7 +692,6 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         }
         running = tot;
     }
-    if (gt == 0) o.row_nnz[i] = running;
     group_bar(bar_id, GT);
     if (CLEAN) {
         // leave the table clean: the key slots of a direct / cuckoo row, else the row's whole table
@@ -708,6 +711,42 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
         }
         group_bar(bar_id, GT);
     }
+    return running;
+}
+
+// A row.  Plain rows whose mask does not fit the largest shared table
+// (cfg5 hubs: up to 163,558 mask entries; the bin's tier-3 launch, see
+// maskmul_abi.cu) are processed in slices of 3/8 of the table's slots of
+// consecutive mask entries: each slice keeps only the
+// products whose column falls in its column range (a sub-range of every
+// sorted B row, found by binary search), so the table stays in shared memory
+// instead of an L2/DRAM-resident global table.  Slices run in column order
+// and append to the row's output, which therefore stays in mask order.
+template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
+__device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
+                                         int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
+                                         BatchSmem bsm, unsigned char* wq,
+                                         unsigned long long& evaluated) {
+    constexpr bool CLEAN = MODE == MODE_PLAIN && SMEM && KIND != 2;
+    const int64_t nm = ri.me - ri.ms;
+    const int64_t w = NUMERIC ? o.off[ri.i] : 0;
+    int64_t total = 0;
+    const int64_t slice = 3ll << (cap_lg_max - 3);   // load 3/8: two-choice cuckoo placement succeeds
+    if (!CLEAN || nm <= slice) {
+        total = hash_part<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, ri.ms, ri.me, INT32_MIN, INT32_MAX, w,
+                                                         cap_lg, cap_lg_max, gt, bar_id, s_warp, bsm, wq,
+                                                         evaluated);
+    } else {
+        for (int64_t s0 = ri.ms; s0 < ri.me; s0 += slice) {
+            const int64_t s1 = s0 + slice < ri.me ? s0 + slice : ri.me;
+            const int32_t c_lo = s0 == ri.ms ? INT32_MIN : p.m_idx[s0];
+            const int32_t c_hi = s1 < ri.me ? p.m_idx[s1] : INT32_MAX;
+            total += hash_part<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, s0, s1, c_lo, c_hi, w + total,
+                                                              cap_lg_max, cap_lg_max, gt, bar_id, s_warp, bsm,
+                                                              wq, evaluated);
+        }
+    }
+    if (gt == 0) o.row_nnz[ri.i] = total;
 }
 
 // ---------------------------------------------------------------------------

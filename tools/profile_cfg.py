@@ -22,5 +22,5 @@ plan = MultiplyPlan(algorithm=algo, semiring=w.semiring, complemented=w.compleme
 for _ in range(reps):
     c, st = multiply_device(dm, da, db, plan, b_csc=bt)
 ms = (C.c_float * 6)(); lib.mm_profile_read(h, ms, 6, None)
-rows = (C.c_int64 * 42)(); fl = (C.c_int64 * 42)(); lib.mm_profile_bins(h, rows, fl, 42)
-print(name, algo, os.environ.get("TUNE", ""), [round(x, 3) for x in ms], {b: (rows[b], fl[b]) for b in range(42) if rows[b]})
+rows = (C.c_int64 * 64)(); fl = (C.c_int64 * 64)(); nb = lib.mm_profile_bins(h, rows, fl, 64)
+print(name, algo, os.environ.get("TUNE", ""), [round(x, 3) for x in ms], {b: (rows[b], fl[b]) for b in range(nb) if rows[b]})
