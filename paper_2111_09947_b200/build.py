@@ -12,7 +12,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(OUT_DIR, "libmaskmul_b200.so")
 SOURCES = ["maskmul_abi.cu"]
 HEADERS = ["common.cuh", "analyze.cuh", "product_loop.cuh", "push_hash.cuh", "push_rank.cuh", "push_heap.cuh", "push_single.cuh", "push_msa_sparse.cuh", "push_dense.cuh",
-           "pull_inner.cuh", "scan_compact.cuh"]
+           "pull_inner.cuh", "scan_compact.cuh", "graph_ops.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -278,19 +278,57 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
             const int slen = plen < 32 ? plen : 0;
             const int sincl = warp_incl_scan(slen, lane32);
             const int stot = __shfl_sync(FULL, sincl, 31);
-            const int sexcl = sincl - slen;
-            for (int w0 = 0; w0 < stot; w0 += 64) {
-                int32_t jj[2];
-                long long ss[2], aa[2];
+            if (stot > 0) {
+#ifndef MM_OWNER_BALLOT
+                const int sexcl = sincl - slen;
+                for (int w0 = 0; w0 < stot; w0 += 64) {
+                    int32_t jj[2];
+                    long long ss[2], aa[2];
 #pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    const int q = w0 + 32 * u + lane32;
-                    const int own = owner_of(sincl, q < stot ? q : stot - 1);
-                    ss[u] = shfl64(sb, own) + (q - __shfl_sync(FULL, sexcl, own));
-                    aa[u] = KIND == 1 ? __shfl_sync(FULL, sa, own) : 0;
-                    jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                    for (int u = 0; u < 2; u++) {
+                        const int q = w0 + 32 * u + lane32;
+                        const int own = owner_of(sincl, q < stot ? q : stot - 1);
+                        ss[u] = shfl64(sb, own) + (q - __shfl_sync(FULL, sexcl, own));
+                        aa[u] = KIND == 1 ? __shfl_sync(FULL, sa, own) : 0;
+                        jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                    }
+                    pr.template put_batch<2>(jj, aa, ss);
                 }
-                pr.template put_batch<2>(jj, aa, ss);
+#else
+                // Owner of each flattened product without a search: the
+                // non-empty short segments are compacted into lanes 0..ns-1
+                // (segment c starts at product c_ex, B slot = c_rel + q).  In
+                // the 32-product window at wb, c0 = the segment holding product
+                // wb (a ballot), and the segments starting inside the window
+                // set bit (start - wb) of S (one REDUX); the owner of product
+                // wb + lane is c0 + popc(S & bits[0..lane]).
+                const int sexcl = sincl - slen;
+                const unsigned nz = __ballot_sync(FULL, slen > 0);
+                const int ns = __popc(nz);
+                const int src = lane32 < ns ? (int)__fns(nz, 0, lane32 + 1) : 0;
+                const long long c_rel = shfl64(sb - sexcl, src);
+                const int ex = __shfl_sync(FULL, sexcl, src);
+                const int c_ex = lane32 < ns ? ex : 0x7fffffff;
+                const long long c_a = KIND == 1 ? shfl64(sa, src) : 0;
+                const unsigned upto = 0xffffffffu >> (31 - lane32);
+                for (int w0 = 0; w0 < stot; w0 += 64) {
+                    int32_t jj[2];
+                    long long ss[2], aa[2];
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        const int wb = w0 + 32 * u;
+                        const int c0 = __popc(__ballot_sync(FULL, c_ex <= wb)) - 1;
+                        const unsigned starts =
+                            __reduce_or_sync(FULL, (c_ex > wb && c_ex < wb + 32) ? 1u << (c_ex - wb) : 0u);
+                        const int own = c0 + __popc(starts & upto);
+                        const int q = wb + lane32;
+                        ss[u] = shfl64(c_rel, own) + q;
+                        aa[u] = KIND == 1 ? shfl64(c_a, own) : 0;
+                        jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
+                    }
+                    pr.template put_batch<2>(jj, aa, ss);
+                }
+#endif
             }
             if (GW == 1) break;
         }

@@ -41,6 +41,7 @@ struct DenseProber {
     uint32_t cnt_s, val_s;
     int32_t lo;
     uint32_t guard;     // index of the guard column
+    uint32_t dummy_s;   // this lane's scratch word (MM_RED_ALL)
     const void* b_val;
     unsigned evaluated;
     template <int U>
@@ -57,12 +58,22 @@ struct DenseProber {
             if (KIND == 0) {
                 // plus-pair: the evaluated count is the sum of the counts, taken at the gather
                 if (NUMERIC)
+#ifndef MM_RED_PRED
+                    asm volatile(
+                        "{\n\t.reg .pred ph;\n\t.reg .u32 ad;\n\t"
+                        "setp.ge.s32 ph, %0, 0;\n\t"
+                        "selp.u32 ad, %1, %2, ph;\n\t"
+                        "red.shared.add.u32 [ad], 1;\n\t}" ::"r"(v[u]),
+                        "r"(cnt_s + (off[u] << 2)), "r"(dummy_s)
+                        : "memory");
+#else
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
                         "setp.ge.s32 ph, %0, 0;\n\t"
                         "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"(v[u]),
                         "r"(cnt_s + (off[u] << 2))
                         : "memory");
+#endif
                 else
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
@@ -154,7 +165,7 @@ __device__ __forceinline__ void dense_gather_comp(const Prob& p, const Out& o, i
 
 template <int GW, int KIND, bool NUMERIC, bool COMP>
 __device__ __forceinline__ void dense_row(const Prob& p, const Out& o, int32_t* cnt, unsigned long long* val,
-                                          int words_max, const RowInfo& ri, int gt, int bar_id, int* s_warp,
+                                          int words_max, uint32_t dummy_s, const RowInfo& ri, int gt, int bar_id, int* s_warp,
                                           BatchSmem bsm, unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
     const int lane = gt & 31;
@@ -204,6 +215,7 @@ __device__ __forceinline__ void dense_row(const Prob& p, const Out& o, int32_t* 
         pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(val);
         pr.lo = lo;
         pr.guard = 32u * (uint32_t)words_max;
+        pr.dummy_s = dummy_s;
         pr.b_val = p.b_val;
         pr.evaluated = 0u;
         flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
@@ -287,6 +299,8 @@ k_push_dense(Prob p, Out o, Work wk, int words_max) {
     int32_t* cnt = (int32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)ncol));
     unsigned char* bbase = smem + (size_t)groups * rbytes + (size_t)g * batch_bytes<GW, KIND>();
     BatchSmem bsm = bind_batch<GW, KIND>(bbase);
+    __shared__ uint32_t s_dummy[256];
+    const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(s_dummy + threadIdx.x);
     for (int c = gt; c < ncol; c += GT) {
         // complement: ALLOWED columns with zero values, the guard DENIED
         cnt[c] = COMP && c < ncol - 1 ? 0 : DENIED;
@@ -297,7 +311,7 @@ k_push_dense(Prob p, Out o, Work wk, int words_max) {
     RowFetcher<GW> rf;
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
-        dense_row<GW, KIND, NUMERIC, COMP>(p, o, cnt, val, words_max, ri, gt, bar_id, s_warp + g * GW, bsm,
+        dense_row<GW, KIND, NUMERIC, COMP>(p, o, cnt, val, words_max, dummy_s, ri, gt, bar_id, s_warp + g * GW, bsm,
                                            evaluated);
     if (NUMERIC) {
         const long long e = warp_sum_ll((long long)evaluated);

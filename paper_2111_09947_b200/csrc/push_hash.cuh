@@ -334,6 +334,7 @@ struct DirectProber {
     uint32_t mult, mult2;
     int shift;            // 32 - lg (direct) or 33 - lg (cuckoo, per half)
     uint32_t half;        // cuckoo: first slot of the upper half
+    uint32_t dummy_s;     // this lane's scratch word
     const void* b_val;
     unsigned evaluated;
     template <int U>
@@ -362,12 +363,24 @@ struct DirectProber {
             if (KIND == 0) {
                 // plus-pair: evaluated = sum of the counts, taken at the gather
                 if (NUMERIC)
+#ifndef MM_RED_PRED
+                    // every lane issues the RED (a miss counts into its own
+                    // dummy word): no branch around the atomic
+                    asm volatile(
+                        "{\n\t.reg .pred ph;\n\t.reg .u32 ad;\n\t"
+                        "setp.ne.u32 ph, %0, 0;\n\t"
+                        "selp.u32 ad, %1, %2, ph;\n\t"
+                        "red.shared.add.u32 [ad], 1;\n\t}" ::"r"((uint32_t)hit),
+                        "r"(cnt_s + (h[u] << 2)), "r"(dummy_s)
+                        : "memory");
+#else
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
                         "setp.ne.u32 ph, %0, 0;\n\t"
                         "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"((uint32_t)hit),
                         "r"(cnt_s + (h[u] << 2))
                         : "memory");
+#endif
                 else
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
@@ -428,7 +441,7 @@ template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
                                          int64_t ms, int64_t me, int32_t c_lo, int32_t c_hi, int64_t w_base,
                                          int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
-                                         BatchSmem bsm, unsigned char* wq,
+                                         BatchSmem bsm, unsigned char* wq, uint32_t dummy_s,
                                          unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
     // Plain masks in shared memory keep the table clean between rows (each
@@ -560,6 +573,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.mult2 = 0u;
         pr.shift = 32 - cap_lg;
         pr.half = 0u;
+        pr.dummy_s = dummy_s;
         pr.b_val = p.b_val;
         pr.evaluated = 0;
         flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
@@ -573,6 +587,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.mult2 = pl.m2;
         pr.shift = 33 - cap_lg;
         pr.half = 1u << (cap_lg - 1);
+        pr.dummy_s = dummy_s;
         pr.b_val = p.b_val;
         pr.evaluated = 0;
         flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
@@ -725,7 +740,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
 template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
                                          int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
-                                         BatchSmem bsm, unsigned char* wq,
+                                         BatchSmem bsm, unsigned char* wq, uint32_t dummy_s,
                                          unsigned long long& evaluated) {
     constexpr bool CLEAN = MODE == MODE_PLAIN && SMEM && KIND != 2;
     const int64_t nm = ri.me - ri.ms;
@@ -735,7 +750,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     if (!CLEAN || nm <= slice) {
         total = hash_part<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, ri.ms, ri.me, INT32_MIN, INT32_MAX, w,
                                                          cap_lg, cap_lg_max, gt, bar_id, s_warp, bsm, wq,
-                                                         evaluated);
+                                                         dummy_s, evaluated);
     } else {
         for (int64_t s0 = ri.ms; s0 < ri.me; s0 += slice) {
             const int64_t s1 = s0 + slice < ri.me ? s0 + slice : ri.me;
@@ -743,7 +758,7 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             const int32_t c_hi = s1 < ri.me ? p.m_idx[s1] : INT32_MAX;
             total += hash_part<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, s0, s1, c_lo, c_hi, w + total,
                                                               cap_lg_max, cap_lg_max, gt, bar_id, s_warp, bsm,
-                                                              wq, evaluated);
+                                                              wq, dummy_s, evaluated);
         }
     }
     if (gt == 0) o.row_nnz[ri.i] = total;
@@ -781,6 +796,8 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
                         (size_t)groups * BATCH_BYTES + (size_t)(threadIdx.x >> 5) * queue_bytes<KIND>();
     Table<KIND> tb;
     tb.bind(base, cap_max);
+    __shared__ uint32_t s_dummy[(GW == 32 ? 32 : (GW == 16 ? 16 : 8)) * 32];
+    const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(s_dummy + threadIdx.x);
     if (MODE == MODE_PLAIN && SMEM && KIND != 2) {   // hash_row keeps it clean from here on
         for (int e = gt; e < cap_max; e += GT) {
             tb.keys[e] = EMPTY_KEY;
@@ -794,7 +811,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
         hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg[ri.i], cap_lg_max, gt, bar_id,
-                                                s_warp + g * GW, bsm, wq, evaluated);
+                                                s_warp + g * GW, bsm, wq, dummy_s, evaluated);
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);
         if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);

@@ -109,6 +109,7 @@ struct MsaProber {
     uint32_t bits_s, cnt_s, val_s;     // bits_s: packed (rank << 16 | 16 column bits) words
     int32_t lo;                        // window start, a multiple of 16
     uint32_t guard;                    // offset of the all-zero guard word (multiple of 16)
+    uint32_t dummy_s;                  // this lane's scratch word (MM_RED_ALL)
     const void* b_val;
     unsigned evaluated;
     // U products at once, stage by stage, so the shared loads of the U
@@ -147,12 +148,24 @@ struct MsaProber {
                 // plus-pair: the evaluated count is the sum of the slot counts,
                 // taken when the row is gathered
                 if (NUMERIC)
+#ifndef MM_RED_PRED
+                    // every lane issues the RED: a miss counts into its own
+                    // dummy word, so ptxas needs no branch around the atomic
+                    asm volatile(
+                        "{\n\t.reg .pred ph;\n\t.reg .u32 ad;\n\t"
+                        "setp.lt.s32 ph, %0, 0;\n\t"
+                        "selp.u32 ad, %1, %2, ph;\n\t"
+                        "red.shared.add.u32 [ad], 1;\n\t}" ::"r"(t),
+                        "r"(cnt_s - 4u + (slot << 2)), "r"(dummy_s)
+                        : "memory");
+#else
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
                         "setp.lt.s32 ph, %0, 0;\n\t"
                         "@ph red.shared.add.u32 [%1], 1;\n\t}" ::"r"(t),
                         "r"(cnt_s - 4u + (slot << 2))
                         : "memory");
+#endif
                 else
                     asm volatile(
                         "{\n\t.reg .pred ph;\n\t"
@@ -229,7 +242,7 @@ __host__ __device__ constexpr int msa_words16(int words_max) { return 2 * (((wor
 
 template <int GW, int KIND, bool MSA, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned char* region, int nm_max,
-                                         int words_max,
+                                         int words_max, uint32_t dummy_s,
                                          const RowInfo& ri, int gt, int bar_id, int* s_warp, BatchSmem bsm,
                                          unsigned long long& evaluated) {
     constexpr int GT = GW * 32;
@@ -307,6 +320,7 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
             pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(sl.val);
             pr.lo = lo;
             pr.guard = (((uint32_t)(hi - lo) >> 4) + 1) << 4;
+            pr.dummy_s = dummy_s;
             pr.b_val = p.b_val;
             pr.evaluated = 0u;
             flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
@@ -396,6 +410,8 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     unsigned char* region = SMEM ? smem + (size_t)g * rbytes : gslab + ((size_t)blockIdx.x * groups + g) * rbytes;
     unsigned char* bbase = smem + (SMEM ? (size_t)groups * rbytes : 0) + (size_t)g * batch_bytes<GW, KIND>();
     BatchSmem bsm = bind_batch<GW, KIND>(bbase);
+    __shared__ uint32_t s_dummy[(GW == 32 ? 32 : (GW == 16 ? 16 : 8)) * 32];
+    const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(s_dummy + threadIdx.x);
     unsigned long long evaluated = 0;
     if (MSA) {
         uint32_t* bits = (uint32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
@@ -404,7 +420,7 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     RowFetcher<GW> rf;
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
-        rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, words_max, ri, gt, bar_id,
+        rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, words_max, dummy_s, ri, gt, bar_id,
                                                s_warp + g * GW, bsm, evaluated);
     if (NUMERIC) {
         const long long e = warp_sum_ll((long long)evaluated);
