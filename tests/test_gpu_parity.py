@@ -21,7 +21,7 @@ import oracle  # noqa: E402
 from golden_util import (digest_csr, digest_mat, load_json, load_npz,  # noqa: E402
                          random_csr, regenerate_random_cases)
 from paper_2111_09947_b200 import (ALGORITHMS, MaskView, MultiplyPlan, PlanError,  # noqa: E402
-                                   SparseError, arithmetic_semiring, from_triples,
+                                   SparseError, arithmetic_semiring, from_arrays, from_triples,
                                    masked_multiply, masked_multiply_with_stats,
                                    plus_pair_semiring, symbolic_phase, workloads)
 from paper_2111_09947_b200.device import DeviceCsr  # noqa: E402
@@ -176,6 +176,39 @@ def test_every_tier_against_oracle(comp):
                 c, st = masked_multiply_with_stats(m.pattern(), aa, bb, plan)
                 assert _digest(c) == want, (rows, algo, sem.name, str(sem.dtype))
                 assert st.evaluated_multiplies == r.evaluated_multiplies
+
+
+@pytest.mark.parametrize("n", [300, 512, 6000])
+def test_narrow_outputs_and_heavy_rows(n):
+    """Heavy rows (tens of thousands of products) into narrow and wide
+    outputs: the complemented dense MSA (every column in shared memory), the
+    column-split ordered float64 groups (4/8/16 warps, bitwise order), 2P."""
+    rng = np.random.default_rng(500 + n)
+    rows = 24
+    blocks = [random_csr(rng, 8, 3000, d) for d in (100, 600, 2500)]   # ~5K / 30K / 100K products per row
+    a = from_arrays(rows, 3000,
+                    np.concatenate([np.repeat(np.arange(8), np.diff(x.row_ptr)) + 8 * q for q, x in enumerate(blocks)]),
+                    np.concatenate([x.col_idx[: x.nnz] for x in blocks]),
+                    np.concatenate([x.values[: x.nnz] for x in blocks]))
+    b = random_csr(rng, 3000, n, min(n / 6, 60))
+    m = random_csr(rng, rows, n, min(n / 4, 150))
+    for comp in (False, True):
+        for sem in (SR, plus_pair_semiring(np.int64), arithmetic_semiring(np.float64)):
+            aa, bb = a, b
+            if sem.dtype == np.float64:
+                aa = a.astype(np.float64)
+                aa.values[:] = rng.standard_normal(aa.nnz)
+                bb = b.astype(np.float64)
+                bb.values[:] = rng.standard_normal(bb.nnz)
+            r = oracle.masked_multiply(m.pattern(), aa, bb, complemented=comp,
+                                       semiring_id=sem.kernel_id, dtype=sem.dtype)
+            want = digest_csr(r.row_ptr, r.col_idx, r.values)
+            for algo in ("msa", "hash", "auto") + (() if comp else ("mca",)):
+                for ph in ("1p", "2p"):
+                    plan = MultiplyPlan(algorithm=algo, phases=ph, complemented=comp, semiring=sem)
+                    c, st = masked_multiply_with_stats(m.pattern(), aa, bb, plan)
+                    assert _digest(c) == want, (n, comp, algo, ph, sem.name, str(sem.dtype))
+                    assert st.evaluated_multiplies == r.evaluated_multiplies
 
 
 def test_determinism_repeat_and_row_partition():
