@@ -135,10 +135,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_inputs(scale):
+def build_inputs(scale, on_device=False):
+    """cfg2's L = tril(relabel(simple(R-MAT edges))).  The edge generator is
+    the host numpy stream (bit-exact with the reference); on_device runs the
+    canonicalisation with the library's own kernels (prep.py), else on the
+    host.  Both give the identical CSR (tests/test_gpu_prep.py)."""
     from paper_2111_09947_b200 import workloads
     t0 = time.perf_counter()
-    low = workloads.triangle_lower(scale)
+    if not on_device:
+        low = workloads.triangle_lower(scale)
+        return low, time.perf_counter() - t0
+    import torch
+    from paper_2111_09947_b200 import prep
+    spec = workloads.GeneratorSpec("rmat", scale, 16, seed=0)
+    src, dst = workloads.rmat_edges(spec)
+    g = prep.simple_undirected_graph(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(), spec.nrows)
+    low = prep.triangle_lower(g).to_host()
     return low, time.perf_counter() - t0
 
 
@@ -226,7 +238,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     _lib.load()
-    low, t_gen = build_inputs(args.scale)
+    low, t_gen = build_inputs(args.scale, on_device=True)
     m = low.nrows
     plan = MultiplyPlan(algorithm=args.algo, semiring=plus_pair_semiring(np.int64))
 

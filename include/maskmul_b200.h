@@ -214,6 +214,33 @@ int mm_ewise_add_end(const mm_matrix_t* a, const mm_matrix_t* b, int dtype, cons
  * src_col[r]] (0 when absent).  src_col may be NULL (no sources). */
 int mm_bc_accumulate(const mm_matrix_t* delta, const int32_t* src_col, double* scores, void* stream);
 
+/* ---- device input preparation (graph_prep.cuh) ---- */
+
+/* flags of mm_csr_from_coo */
+enum { MM_COO_SYMMETRIC = 1, MM_COO_NO_DIAG = 2, MM_COO_LOWER = 4, MM_COO_DEDUP = 8 };
+
+/* from_arrays / _canonical_from_sorted_triples (sparse.py:190-244) on the
+ * device: COO (rows, cols: int64 when idx64 else int32; nnz entries) -> CSR
+ * with rows sorted by column.  map (optional, int32[n]) relabels both
+ * endpoints first (permute_symmetric, sparse.py:318-325).  MM_COO_SYMMETRIC
+ * also emits (c, r); MM_COO_NO_DIAG drops r == c; MM_COO_LOWER keeps c < r
+ * (tril_strict, sparse.py:285-291); MM_COO_DEDUP merges duplicates
+ * (pattern only: simple_undirected_graph, sparse.py:344-357).  vals
+ * (optional 8-byte payload per entry, not with DEDUP) travel with the columns
+ * into out_vals.  out_idx / out_vals need capacity nnz (2 nnz when
+ * symmetrising); *out_nnz (host) receives the entry count.  Synchronous. */
+int mm_csr_from_coo(int64_t nrows, int64_t ncols, const void* rows, const void* cols, int idx64, int64_t nnz,
+                    const int32_t* map, int flags, const void* vals, int64_t* out_ptr, int32_t* out_idx,
+                    void* out_vals, int64_t* out_nnz, void* stream);
+
+/* Row id of every CSR entry: rows[t] = i for ptr[i] <= t < ptr[i+1]. */
+int mm_expand_rows(int64_t nrows, const int64_t* ptr, int32_t* rows, void* stream);
+
+/* degree_sort_relabel's permutation (sparse.py:328-341): perm[new] = old in
+ * non-increasing degree order, ties by index; new_label[old] = new.
+ * Synchronous (reads the maximum degree back). */
+int mm_degree_order(const mm_matrix_t* g, int32_t* perm, int32_t* new_label, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,8 @@ EXPORTS = ("mm_abi_version", "mm_last_error", "mm_create", "mm_destroy", "mm_mul
            "mm_compact_rows", "mm_reduce_sum", "mm_profile_enable", "mm_profile_read",
            "mm_profile_bins", "mm_set_tuning", "mm_filter_min", "mm_lookup_rows",
            "mm_bc_dependency_weights", "mm_bc_scale_by", "mm_ewise_add_begin", "mm_ewise_add_end",
-           "mm_bc_accumulate")
+           "mm_bc_accumulate", "mm_csr_from_coo", "mm_expand_rows", "mm_degree_order")
+MM_COO_SYMMETRIC, MM_COO_NO_DIAG, MM_COO_LOWER, MM_COO_DEDUP = 1, 2, 4, 8
 
 
 class MatrixT(C.Structure):
@@ -76,6 +77,10 @@ def load(path: str | None = None):
     lib.mm_ewise_add_begin.argtypes = [PM, PM, P, C.POINTER(C.c_int64), P]
     lib.mm_ewise_add_end.argtypes = [PM, PM, C.c_int, P, P, P, P]
     lib.mm_bc_accumulate.argtypes = [PM, P, P, P]
+    lib.mm_csr_from_coo.argtypes = [C.c_int64, C.c_int64, P, P, C.c_int, C.c_int64, P, C.c_int, P, P, P, P,
+                                    C.POINTER(C.c_int64), P]
+    lib.mm_expand_rows.argtypes = [C.c_int64, P, P, P]
+    lib.mm_degree_order.argtypes = [PM, P, P, P]
     for name in EXPORTS:
         getattr(lib, name)
         if name not in ("mm_last_error",):

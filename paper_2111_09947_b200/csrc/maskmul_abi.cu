@@ -28,6 +28,7 @@
 #include "push_dense.cuh"
 #include "scan_compact.cuh"
 #include "graph_ops.cuh"
+#include "graph_prep.cuh"
 
 using namespace mm;
 
@@ -1191,5 +1192,175 @@ int mm_bc_accumulate(const mm_matrix_t* delta, const int32_t* src_col, double* s
     return MM_OK;
 }
 
+// ---- device input preparation (graph_prep.cuh) ----
+
+int mm_expand_rows(int64_t nrows, const int64_t* ptr, int32_t* rows, void* stream) {
+    if (nrows <= 0) return MM_OK;
+    if (!ptr || !rows) return fail(MM_ERR_INPUT, "null argument");
+    ++g_launches;
+    k_expand_rows<<<warp_grid(nrows), 256, 0, (cudaStream_t)stream>>>(nrows, ptr, rows);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+static int read_i64(const void* dptr, int64_t* out, cudaStream_t st) {
+    long long* h = nullptr;
+    cudaError_t e = cudaMallocHost((void**)&h, sizeof(long long));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, dptr, sizeof(long long), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) *out = *h;
+    if (h) cudaFreeHost(h);
+    if (e != cudaSuccess) return fail(MM_ERR_CUDA, std::string("readback: ") + cudaGetErrorString(e));
+    return MM_OK;
+}
+
+// Sort every segment [ptr[s], ptr[s+1]) of keys (and 8-byte vals) ascending.
+static int segmented_sort(int64_t nseg, const int64_t* ptr, int32_t* keys, unsigned long long* vals,
+                          cudaStream_t st) {
+    if (nseg <= 0) return MM_OK;
+    int32_t* big = nullptr;
+    unsigned long long* mx = nullptr;
+    CU(cudaMallocAsync((void**)&big, nseg * sizeof(int32_t) + 16, st));
+    CU(cudaMallocAsync((void**)&mx, 2 * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(mx, 0, 2 * sizeof(unsigned long long), st));
+    int* nbig = (int*)(mx + 1);
+    ++g_launches;
+    if (vals) k_seg_sort_warp<true><<<warp_grid(nseg), 256, 0, st>>>(nseg, ptr, keys, vals, big, nbig);
+    else k_seg_sort_warp<false><<<warp_grid(nseg), 256, 0, st>>>(nseg, ptr, keys, vals, big, nbig);
+    ++g_launches;
+    k_max_degree<<<(int)std::min<int64_t>((nseg + 255) / 256, 148 * 8), 256, 0, st>>>(nseg, ptr, mx);
+    int64_t hv[2] = {0, 0};
+    {
+        long long* h = nullptr;
+        cudaError_t e = cudaMallocHost((void**)&h, 2 * sizeof(long long));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, mx, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) { hv[0] = h[0]; hv[1] = h[1]; }
+        if (h) cudaFreeHost(h);
+        if (e != cudaSuccess) { cudaFreeAsync(big, st); cudaFreeAsync(mx, st); return fail(MM_ERR_CUDA, cudaGetErrorString(e)); }
+    }
+    const int64_t maxlen = hv[0];
+    const int nb = (int)(hv[1] & 0xffffffff);
+    if (nb > 0) {
+        int64_t P = 1;
+        while (P < maxlen) P <<= 1;
+        const int64_t cap = P > PREP_TILE ? P : 0;
+        const int grid = (int)std::min<int64_t>(nb, 148 * 2);
+        int32_t* sk = nullptr;
+        unsigned long long* sv = nullptr;
+        if (cap) {
+            CU(cudaMallocAsync((void**)&sk, (size_t)grid * cap * sizeof(int32_t), st));
+            if (vals) CU(cudaMallocAsync((void**)&sv, (size_t)grid * cap * sizeof(unsigned long long), st));
+        }
+        ++g_launches;
+        if (vals) k_seg_sort_block<true><<<grid, PREP_THREADS, 0, st>>>(ptr, keys, vals, big, nbig, sk, sv, cap);
+        else k_seg_sort_block<false><<<grid, PREP_THREADS, 0, st>>>(ptr, keys, vals, big, nbig, sk, sv, cap);
+        if (sk) cudaFreeAsync(sk, st);
+        if (sv) cudaFreeAsync(sv, st);
+    }
+    cudaFreeAsync(big, st);
+    cudaFreeAsync(mx, st);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
+int mm_csr_from_coo(int64_t nrows, int64_t ncols, const void* rows, const void* cols, int idx64, int64_t nnz,
+                    const int32_t* map, int flags, const void* vals, int64_t* out_ptr, int32_t* out_idx,
+                    void* out_vals, int64_t* out_nnz, void* stream) {
+    if (!out_ptr || !out_nnz || (nnz > 0 && (!rows || !cols || !out_idx))) return fail(MM_ERR_INPUT, "null argument");
+    if (nrows < 0 || ncols < 0 || nrows >= (1ll << 31) || ncols >= (1ll << 31))
+        return fail(MM_ERR_INPUT, "dimensions must be in [0, 2^31)");
+    const bool dedup = flags & MM_COO_DEDUP;
+    if ((flags & MM_COO_SYMMETRIC) && nrows != ncols) return fail(MM_ERR_INPUT, "symmetrising needs a square matrix");
+    if (dedup && vals) return fail(MM_ERR_INPUT, "duplicate merging is pattern-only");
+    cudaStream_t st = (cudaStream_t)stream;
+    CooView v{rows, cols, idx64, map, (flags & MM_COO_SYMMETRIC) ? 1 : 0, (flags & MM_COO_NO_DIAG) ? 1 : 0,
+              (flags & MM_COO_LOWER) ? 1 : 0, nnz};
+    const int64_t cap = nnz * (v.sym ? 2 : 1);
+    int64_t* counts = nullptr;
+    int64_t* tptr = nullptr;
+    CU(cudaMallocAsync((void**)&counts, (nrows + 2) * sizeof(int64_t), st));
+    CU(cudaMallocAsync((void**)&tptr, (nrows + 2) * sizeof(int64_t), st));
+    CU(cudaMemsetAsync(counts, 0, (nrows + 1) * sizeof(int64_t), st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nnz + 255) / 256, 148 * 16));
+    if (nnz > 0) {
+        ++g_launches;
+        k_coo_count<<<grid, 256, 0, st>>>(v, counts);
+    }
+    int64_t* dst_ptr = dedup ? tptr : out_ptr;
+    int rc = exclusive_scan(counts, nrows, dst_ptr, st);
+    int32_t* kidx = out_idx;
+    if (!rc && dedup) {
+        if (cudaMallocAsync((void**)&kidx, std::max<int64_t>(cap, 1) * sizeof(int32_t), st) != cudaSuccess)
+            rc = fail(MM_ERR_CUDA, "cudaMallocAsync failed");
+    }
+    if (!rc && nnz > 0) {
+        // cursors start at the row offsets (counts is reused as the cursor array)
+        cudaMemcpyAsync(counts, dst_ptr, nrows * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+        ++g_launches;
+        k_coo_scatter<<<grid, 256, 0, st>>>(v, (const unsigned long long*)vals, (unsigned long long*)counts, kidx,
+                                            (unsigned long long*)out_vals);
+        rc = segmented_sort(nrows, dst_ptr, kidx, (unsigned long long*)(vals ? out_vals : nullptr), st);
+    }
+    if (!rc && dedup) {
+        if (nrows > 0) {
+            ++g_launches;
+            k_unique_count<<<warp_grid(nrows), 256, 0, st>>>(nrows, tptr, kidx, counts);
+        }
+        rc = exclusive_scan(counts, nrows, out_ptr, st);
+        if (!rc && nrows > 0) {
+            ++g_launches;
+            k_unique_compact<<<warp_grid(nrows), 256, 0, st>>>(nrows, tptr, kidx, out_ptr, out_idx);
+        }
+    }
+    if (!rc) rc = read_i64(out_ptr + nrows, out_nnz, st);
+    if (dedup && kidx && kidx != out_idx) cudaFreeAsync(kidx, st);
+    cudaFreeAsync(counts, st);
+    cudaFreeAsync(tptr, st);
+    if (!rc) CU(cudaGetLastError());
+    return rc;
+}
+
+int mm_degree_order(const mm_matrix_t* g, int32_t* perm, int32_t* new_label, void* stream) {
+    if (!g || !g->ptr || !perm || !new_label) return fail(MM_ERR_INPUT, "null argument");
+    if (g->nrows != g->ncols) return fail(MM_ERR_INPUT, "degree_sort_relabel requires a square matrix");
+    const int64_t n = g->nrows;
+    if (n == 0) return MM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* mx = nullptr;
+    CU(cudaMallocAsync((void**)&mx, sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    ++g_launches;
+    k_max_degree<<<grid, 256, 0, st>>>(n, g->ptr, mx);
+    int64_t maxdeg = 0;
+    int rc = read_i64(mx, &maxdeg, st);
+    cudaFreeAsync(mx, st);
+    if (rc) return rc;
+    int64_t* hist = nullptr;
+    int64_t* bptr = nullptr;
+    CU(cudaMallocAsync((void**)&hist, (maxdeg + 2) * sizeof(int64_t), st));
+    CU(cudaMallocAsync((void**)&bptr, (maxdeg + 3) * sizeof(int64_t), st));
+    CU(cudaMemsetAsync(hist, 0, (maxdeg + 1) * sizeof(int64_t), st));
+    ++g_launches;
+    k_degree_hist<<<grid, 256, 0, st>>>(n, g->ptr, maxdeg, hist);
+    rc = exclusive_scan(hist, maxdeg + 1, bptr, st);
+    if (!rc) {
+        cudaMemcpyAsync(hist, bptr, (maxdeg + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+        ++g_launches;
+        k_degree_scatter<<<grid, 256, 0, st>>>(n, g->ptr, maxdeg, (unsigned long long*)hist, perm);
+        rc = segmented_sort(maxdeg + 1, bptr, perm, nullptr, st);   // ids ascending inside a degree
+    }
+    if (!rc) {
+        ++g_launches;
+        k_invert_perm<<<grid, 256, 0, st>>>(n, perm, new_label);
+    }
+    cudaFreeAsync(hist, st);
+    cudaFreeAsync(bptr, st);
+    if (!rc) CU(cudaGetLastError());
+    return rc;
+}
+
 }  // extern "C"
+
 

@@ -92,16 +92,10 @@ class DeviceCsr:
         """CSR -> CSC of the same matrix (to_csc, sparse.py:257-266): stable
         order, so row indices ascend inside every column.  Input preparation
         for the pull path (the reference excludes it from timing,
-        multiply.py:205-210); runs on the device with torch sort."""
+        multiply.py:205-210); runs on the device (prep.transpose: row scatter
+        by column + segmented sort, csrc/graph_prep.cuh)."""
         if self.csc:
             raise SparseError("already column-major")
-        dev = self.idx.device
-        rows = torch.repeat_interleave(torch.arange(self.nrows, device=dev, dtype=torch.int32),
-                                       torch.diff(self.ptr))
-        cols = self.idx.to(torch.int64)
-        order = torch.argsort(cols, stable=True)
-        counts = torch.bincount(cols, minlength=self.ncols)
-        col_ptr = torch.zeros(self.ncols + 1, dtype=torch.int64, device=dev)
-        col_ptr[1:] = torch.cumsum(counts, 0)
-        vals = self.values[order] if self.values is not None else None
-        return DeviceCsr(self.nrows, self.ncols, col_ptr, rows[order].contiguous(), vals, csc=True)
+        from .prep import transpose
+        t = transpose(self)
+        return DeviceCsr(self.nrows, self.ncols, t.ptr, t.idx, t.values, csc=True)

@@ -20,8 +20,7 @@ import numpy as np
 from .device import DeviceCsr
 from .multiply import MultiplyPlan, PlanError, multiply_device, reduce_sum
 from .semiring import arithmetic_semiring, plus_pair_semiring
-from .sparse import (CsrMatrix, SparseError, degree_sort_relabel, from_arrays,
-                     is_pattern_symmetric, tril_strict)
+from .sparse import CsrMatrix, SparseError, is_pattern_symmetric
 
 
 @dataclass(frozen=True)
@@ -62,10 +61,12 @@ def _check_simple_symmetric(g: CsrMatrix, what: str) -> None:
 
 
 def triangle_count(g: CsrMatrix, plan: MultiplyPlan, device=None) -> KernelResult:
+    """graphs.py:87-96.  The relabel + strict lower triangle run on the device
+    (prep.triangle_lower, identical to the host tril_strict(degree_sort_relabel))."""
+    from . import prep
     _check_simple_symmetric(g, "triangle counting")
-    low = tril_strict(degree_sort_relabel(g)[0])
     kplan = replace(plan, semiring=plus_pair_semiring(np.int64), complemented=False)
-    dl = DeviceCsr.from_host(low, device=device, with_values=False)
+    dl = prep.triangle_lower(DeviceCsr.from_host(g, device=device, with_values=False))
     c, st = multiply_device(dl, dl, dl, kplan,
                             b_csc=dl.transpose_storage() if kplan.algorithm == "inner" else None)
     total = int(reduce_sum(c.values).item()) if c.nnz else 0

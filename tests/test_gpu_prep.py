@@ -1,0 +1,78 @@
+"""Device input preparation against the host functions,
+which mirror the reference (sparse.py:223-357): identical canonical CSR and
+identical permutation, on random COO lists with duplicates and self-loops, on
+R-MAT graphs (cfg2's s20 graph included, pinned by the golden digest), and on
+segments long enough for the block / global bitonic paths."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from golden_util import digest_mat, load_json  # noqa: E402
+from paper_2111_09947_b200 import prep  # noqa: E402
+from paper_2111_09947_b200.device import DeviceCsr  # noqa: E402
+from paper_2111_09947_b200.sparse import (degree_sort_relabel, from_arrays, simple_undirected_graph,  # noqa: E402
+                                          to_csc, tril_strict)
+from paper_2111_09947_b200.workloads import GeneratorSpec, generate, rmat_edges, simple_graph_direct  # noqa: E402
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def _same(dev: DeviceCsr, host):
+    h = dev.to_host()
+    assert np.array_equal(h.row_ptr, host.row_ptr)
+    assert np.array_equal(h.col_idx[: h.nnz], host.col_idx[: host.nnz])
+
+
+@pytest.mark.parametrize("n,m,hub", [(50, 400, 0), (3000, 40000, 0), (2000, 60000, 9000), (70000, 300000, 80000)])
+def test_simple_undirected_graph_matches_host(n, m, hub):
+    rng = np.random.default_rng(n + m)
+    r = rng.integers(0, n, m)
+    c = rng.integers(0, n, m)
+    if hub:   # one vertex with a long row: block and global bitonic paths
+        r[:hub] = 0
+        c[:hub] = rng.integers(0, n, hub)
+    want = simple_undirected_graph(from_arrays(n, n, r, c, np.ones(m, dtype=np.int64)))
+    got = prep.simple_undirected_graph(r, c, n)
+    _same(got, want)
+
+
+@pytest.mark.parametrize("scale", [8, 12, 16])
+def test_relabel_tril_transpose_match_host(scale):
+    g = simple_graph_direct(GeneratorSpec("rmat", scale, 16, seed=scale))
+    dg = DeviceCsr.from_host(g, with_values=False)
+    rl, perm = degree_sort_relabel(g)
+    drl, dperm = prep.degree_sort_relabel(dg)
+    assert np.array_equal(dperm.cpu().numpy(), perm)
+    _same(drl, rl)
+    _same(prep.tril_strict(drl), tril_strict(rl))
+    _same(prep.triangle_lower(dg), tril_strict(rl))
+    # transpose with values (8-byte payload follows its entry)
+    a = generate(GeneratorSpec("erdos-renyi", scale, 8, seed=scale)).astype(np.float64)
+    a.values[:] = np.random.default_rng(scale).standard_normal(a.nnz)
+    da = DeviceCsr.from_host(a, dtype=np.float64)
+    t = da.transpose_storage()
+    want = to_csc(a)
+    assert np.array_equal(t.ptr.cpu().numpy(), want.col_ptr)
+    assert np.array_equal(t.idx.cpu().numpy(), want.row_idx[: want.nnz])
+    assert np.array_equal(t.values.cpu().numpy(), want.values[: want.nnz])
+
+
+def test_cfg2_input_pipeline_on_device():
+    """R-MAT s20 edges (host generator) -> simple graph -> relabel -> tril on
+    the device gives cfg2's L bit for bit (golden input digest)."""
+    spec = GeneratorSpec("rmat", 20, 16, seed=0)
+    src, dst = rmat_edges(spec)
+    g = prep.simple_undirected_graph(src, dst, spec.nrows)
+    low = prep.triangle_lower(g).to_host()
+    want = load_json("configs.json")["cfg2"]["digest_m"]   # the pattern of L
+    low.values = None
+    assert digest_mat(low) == want
