@@ -36,6 +36,14 @@ namespace {
 
 thread_local std::string g_last_error;
 thread_local long long g_launches = 0;   // kernels launched by this thread (profiling)
+thread_local long long* g_pinned = nullptr;  // 4 pinned words for small synchronous readbacks
+
+// Pinned host scratch for the free-standing calls' readbacks (allocated once
+// per thread: cudaMallocHost per call costs more than the work it reads).
+long long* pinned_scratch() {
+    if (!g_pinned && cudaMallocHost((void**)&g_pinned, 4 * sizeof(long long)) != cudaSuccess) g_pinned = nullptr;
+    return g_pinned;
+}
 
 bool debug_launches() {
     static int on = -1;
@@ -57,6 +65,19 @@ int fail(int code, const std::string& msg) {
         if (_e != cudaSuccess)                                                            \
             return fail(MM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
     } while (0)
+
+// Small synchronous readback of n int64 words through the pinned scratch.
+int read_i64s(const void* dptr, int64_t* out, int n, cudaStream_t st) {
+    long long* h = pinned_scratch();
+    if (!h) return fail(MM_ERR_CUDA, "cudaMallocHost failed");
+    cudaError_t e = cudaMemcpyAsync(h, dptr, n * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(MM_ERR_CUDA, std::string("readback: ") + cudaGetErrorString(e));
+    for (int q = 0; q < n; q++) out[q] = h[q];
+    return MM_OK;
+}
+
+int read_i64(const void* dptr, int64_t* out, cudaStream_t st) { return read_i64s(dptr, out, 1, st); }
 
 }  // namespace
 
@@ -1030,9 +1051,9 @@ int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t m = c->nrows;
     int64_t* counts = nullptr;
-    long long* hnz = nullptr;
+    long long* hnz = pinned_scratch();
+    if (!hnz) return fail(MM_ERR_CUDA, "cudaMallocHost failed");
     CU(cudaMallocAsync((void**)&counts, std::max<int64_t>(m, 1) * sizeof(int64_t), st));
-    CU(cudaMallocHost((void**)&hnz, sizeof(long long)));
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 7) / 8, 148 * 16));
     if (m > 0) {
         ++g_launches;
@@ -1040,7 +1061,7 @@ int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32
                                                   nullptr, nullptr);
     }
     int rc = exclusive_scan(counts, m, out_row_ptr, st);
-    if (rc) { cudaFreeAsync(counts, st); cudaFreeHost(hnz); return rc; }
+    if (rc) { cudaFreeAsync(counts, st); return rc; }
     if (m > 0) {
         ++g_launches;
         k_filter_min<true><<<grid, 256, 0, st>>>(m, c->ptr, c->idx, (const long long*)c->values, thr, nullptr,
@@ -1050,7 +1071,6 @@ int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32
     CU(cudaStreamSynchronize(st));
     *out_nnz = *hnz;
     cudaFreeAsync(counts, st);
-    cudaFreeHost(hnz);
     CU(cudaGetLastError());
     return MM_OK;
 }
@@ -1145,15 +1165,7 @@ int mm_ewise_add_begin(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* c_ro
         k_ewise_count<<<warp_grid(m), 256, 0, st>>>(m, a->ptr, a->idx, b->ptr, b->idx, counts);
     }
     int rc = exclusive_scan(counts, m, c_row_ptr, st, nullptr, nullptr, nullptr, total);
-    long long* h = nullptr;
-    if (!rc) {
-        cudaError_t e = cudaMallocHost((void**)&h, sizeof(long long));
-        if (e == cudaSuccess) e = cudaMemcpyAsync(h, total, sizeof(long long), cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) rc = fail(MM_ERR_CUDA, std::string("ewise_add count readback: ") + cudaGetErrorString(e));
-        else *nnz = *h;
-    }
-    if (h) cudaFreeHost(h);
+    if (!rc) rc = read_i64(total, nnz, st);
     cudaFreeAsync(counts, st);
     return rc;
 }
@@ -1203,16 +1215,6 @@ int mm_expand_rows(int64_t nrows, const int64_t* ptr, int32_t* rows, void* strea
     return MM_OK;
 }
 
-static int read_i64(const void* dptr, int64_t* out, cudaStream_t st) {
-    long long* h = nullptr;
-    cudaError_t e = cudaMallocHost((void**)&h, sizeof(long long));
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h, dptr, sizeof(long long), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e == cudaSuccess) *out = *h;
-    if (h) cudaFreeHost(h);
-    if (e != cudaSuccess) return fail(MM_ERR_CUDA, std::string("readback: ") + cudaGetErrorString(e));
-    return MM_OK;
-}
 
 // Sort every segment [ptr[s], ptr[s+1]) of keys (and 8-byte vals) ascending.
 static int segmented_sort(int64_t nseg, const int64_t* ptr, int32_t* keys, unsigned long long* vals,
@@ -1230,14 +1232,10 @@ static int segmented_sort(int64_t nseg, const int64_t* ptr, int32_t* keys, unsig
     ++g_launches;
     k_max_degree<<<(int)std::min<int64_t>((nseg + 255) / 256, 148 * 8), 256, 0, st>>>(nseg, ptr, mx);
     int64_t hv[2] = {0, 0};
-    {
-        long long* h = nullptr;
-        cudaError_t e = cudaMallocHost((void**)&h, 2 * sizeof(long long));
-        if (e == cudaSuccess) e = cudaMemcpyAsync(h, mx, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e == cudaSuccess) { hv[0] = h[0]; hv[1] = h[1]; }
-        if (h) cudaFreeHost(h);
-        if (e != cudaSuccess) { cudaFreeAsync(big, st); cudaFreeAsync(mx, st); return fail(MM_ERR_CUDA, cudaGetErrorString(e)); }
+    if (int rc = read_i64s(mx, hv, 2, st)) {
+        cudaFreeAsync(big, st);
+        cudaFreeAsync(mx, st);
+        return rc;
     }
     const int64_t maxlen = hv[0];
     const int nb = (int)(hv[1] & 0xffffffff);
