@@ -416,6 +416,7 @@ def run_ours(args, rank, world, local_rank):
             "hbm_alg_gbs": bytes_alg / (ms_max * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "frac_of_8tbs": achieved / 8000.0,      # north_star's denominator
                          "kernel": "numeric phase: every row-bin kernel of one multiply (MSA bitmap / hash / pull tiers)",
                          "bytes_alg_per_launch": bytes_alg, "kernel_ms": numeric_ms,
                          "peak_source": peak_src,

@@ -746,7 +746,11 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     const int64_t nm = ri.me - ri.ms;
     const int64_t w = NUMERIC ? o.off[ri.i] : 0;
     int64_t total = 0;
-    const int64_t slice = 3ll << (cap_lg_max - 3);   // load 3/8: two-choice cuckoo placement succeeds
+#ifndef MM_SLICE_EIGHTHS
+#define MM_SLICE_EIGHTHS 3
+#endif
+    // load 3/8 of the table: two-choice cuckoo placement succeeds
+    const int64_t slice = (int64_t)MM_SLICE_EIGHTHS << (cap_lg_max - 3);
     if (!CLEAN || nm <= slice) {
         total = hash_part<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, ri.ms, ri.me, INT32_MIN, INT32_MAX, w,
                                                          cap_lg, cap_lg_max, gt, bar_id, s_warp, bsm, wq,
