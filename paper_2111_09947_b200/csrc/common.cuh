@@ -36,6 +36,7 @@ struct Out {
     int64_t* row_nnz;
     unsigned long long* evaluated;
     int out_f64;  // 1: values are float64, 0: int64
+    int* overflow;  // small-problem path: set when a row does not fit the fixed table (host falls back)
 };
 
 // A bin of rows handled by one kernel family/tier, fetched dynamically.

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -43,6 +44,34 @@ thread_local long long* g_pinned = nullptr;  // 4 pinned words for small synchro
 long long* pinned_scratch() {
     if (!g_pinned && cudaMallocHost((void**)&g_pinned, 4 * sizeof(long long)) != cudaSuccess) g_pinned = nullptr;
     return g_pinned;
+}
+
+// MM_HOST_TRACE=1: host-side timestamps of one multiply's steps (stderr).
+bool host_trace() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MM_HOST_TRACE");
+        on = e && *e && *e != '0';
+    }
+    return on == 1;
+}
+thread_local std::chrono::steady_clock::time_point g_t0;
+thread_local char g_trace[512];
+thread_local int g_trace_len = 0;
+void trace(const char* what) {
+    if (!host_trace()) return;
+    const auto now = std::chrono::steady_clock::now();
+    if (what[0] == '^') {
+        g_t0 = now;
+        g_trace_len = 0;
+        what++;
+    }
+    const double us = std::chrono::duration<double, std::micro>(now - g_t0).count();
+    g_trace_len += snprintf(g_trace + g_trace_len, sizeof(g_trace) - g_trace_len, " %s=%.1f", what, us);
+    if (what[0] == '$') {
+        fprintf(stderr, "[mm trace]%s\n", g_trace);
+        g_trace_len = 0;
+    }
 }
 
 bool debug_launches() {
@@ -122,6 +151,7 @@ struct mm_handle {
     int rank_budget[3] = {6144, 24576, 49152};
     int auto_mca_nm = 0;
     int direct_lg[3] = {9, 10, 12};    // plain shared hash tables per tier: at least 2^direct_lg slots (0 = bin size)
+    int64_t tiny_rows = 1 << 15, tiny_nnz = 1 << 20;   // single-pass path for small plain 1P multiplies
     // ---- concurrent bin launches ----
     static constexpr int NAUX = 3;
     cudaStream_t aux[NAUX] = {};
@@ -615,6 +645,7 @@ int sync_read(mm_handle* h, void* dst, const void* src, size_t bytes) {
 int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
                const mm_matrix_t* b, const mm_matrix_t* bt, cudaStream_t st, bool symbolic_only,
                int64_t* counts_out, int64_t* out_nnz) {
+    trace("^begin");
     int rc = validate(plan, mask, a, b, bt);
     if (rc) return rc;
     if (h->active) release(h);
@@ -702,6 +733,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     h->tmp_idx = plain_1p ? (int32_t*)(slab + o_tidx) : nullptr;
     h->tmp_val = plain_1p ? (void*)(slab + o_tval) : nullptr;
     p.row_flops = h->row_flops;
+    trace("slab");
     CU(cudaMemsetAsync(h->d_summary, 0, zero_bytes, st));
 
     if (m > 0) {
@@ -719,6 +751,67 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
             CU(cudaGetLastError());
         }
     }
+    // ---- small plain one-phase problems: one pass over every row with a
+    // fixed single-warp table, one host sync (no binning round trip).  A row
+    // whose mask does not fit sets the overflow flag and the multiply falls
+    // back to the binned path below (the analysis summary is already there).
+    const bool tiny = plain_1p && m > 0 && m <= h->tiny_rows && mask->nnz <= h->tiny_nnz &&
+                      a->nnz <= h->tiny_nnz &&
+                      (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH ||
+                       plan->algorithm == MM_ALGO_MSA || plan->algorithm == MM_ALGO_MCA);
+    bool have_summary = false;
+    if (tiny) {
+        h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
+        Out o{};
+        o.off = h->bound_off;
+        o.idx = h->tmp_idx;
+        o.val = h->tmp_val;
+        o.row_nnz = h->row_nnz;
+        o.evaluated = &h->d_summary->evaluated;
+        o.out_f64 = h->out_f64;
+        o.overflow = &h->d_summary->pad;
+        int gw = 1;
+        HashKernel kern = pick_hash(h->kind, MODE_PLAIN, 0, true, &gw);
+        const int cap_lg = h->kind == 0 ? 10 : 9;
+        const size_t ebytes = h->kind == 0 ? 8 : 16;
+        const size_t queue = h->kind == 2 ? 0 : (size_t)64 * (h->kind == 1 ? 24 : 8);
+        const size_t smem = 8 * (((size_t)1 << cap_lg) * ebytes + batch_bytes_rt(1, h->kind)) + 8 * queue;
+        int occ = 0;
+        if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
+        const int grid = std::max(1, std::min((int)((m + 7) / 8), std::max(occ, 1) * h->num_sms));
+        Work wk{nullptr, (int32_t)m, h->cursors + 2 * NBINS};
+        ++g_launches;
+        kern<<<grid, 256, smem, st>>>(h->prob, o, wk, nullptr, cap_lg, nullptr);
+        CU(cudaGetLastError());
+        if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st, h->scan_scratch, h->bound_off,
+                                 &h->d_summary->flag, &h->d_summary->total_nnz)))
+            return rc;
+        trace("tiny");
+        if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+        have_summary = true;
+        if (!h->h_summary->pad) {
+            h->sum = *h->h_summary;
+            mark(h, 1);
+            mark(h, 2);
+            mark(h, 3);
+            h->stats = mm_stats_t{};
+            h->stats.generated_flops = (int64_t)h->sum.gen_flops;
+            h->stats.rows_empty = h->sum.bin_count[BIN_EMPTY];
+            h->stats.rows_push = m - h->stats.rows_empty;
+            h->total_nnz = h->sum.total_nnz;
+            h->stats.evaluated_multiplies = (int64_t)h->sum.evaluated;
+            h->bound_flag = h->sum.flag;
+            trace("sync2");
+            mark(h, 4);
+            *out_nnz = h->total_nnz;
+            h->active = true;
+            return MM_OK;
+        }
+        // fallback: forget what the single pass accumulated
+        CU(cudaMemsetAsync(&h->d_summary->evaluated, 0, sizeof(h->d_summary->evaluated), st));
+        CU(cudaMemsetAsync(h->cursors + 2 * NBINS, 0, NBINS * sizeof(int32_t), st));
+        h->h_summary->evaluated = 0;
+    }
     if (m > 0) {
         // the scatter reads the bin counts from the device summary, so it is
         // queued before the host waits for that summary (one launch gap fewer)
@@ -727,7 +820,9 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
         k_bin_scatter<<<grid, 256, 0, st>>>(m, h->row_bin, h->d_summary, h->cursors, h->rows_list);
         CU(cudaGetLastError());
     }
-    if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+    trace("launched");
+    if (!have_summary && (rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+    trace("sync1");
     h->sum = *h->h_summary;
     mark(h, 1);
     h->bin_off[0] = 0;
@@ -779,6 +874,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     o.evaluated = &h->d_summary->evaluated;
     o.out_f64 = h->out_f64;
     if ((rc = launch_bins(h, true, o))) return rc;
+    trace("bins");
     mark(h, 3);
     // the bound assertion (multiply.py:390) is folded into the scan and rides
     // on the nnz readback below
@@ -789,6 +885,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     h->total_nnz = h->h_summary->total_nnz;
     h->stats.evaluated_multiplies = (int64_t)h->h_summary->evaluated;
     h->bound_flag = h->h_summary->flag;
+    trace("sync2");
     mark(h, 4);
     *out_nnz = h->total_nnz;
     h->active = true;
@@ -797,6 +894,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
 
 int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_values, mm_stats_t* stats) {
     if (!h->active) return fail(MM_ERR_INPUT, "mm_multiply_end without a successful mm_multiply_begin");
+    trace("end");
     cudaStream_t st = h->stream;
     const int64_t m = h->nrows;
     int rc;
@@ -842,6 +940,7 @@ int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_value
         if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) { release(h); return rc; }
         h->stats.evaluated_multiplies = (int64_t)h->h_summary->evaluated;
     }
+    trace("$done");
     int bad = h->plan.phases == 1 ? h->bound_flag : h->h_summary->flag;
     h->launches = g_launches - h->launch_base;
     h->stats.output_nnz = h->total_nnz;
@@ -949,6 +1048,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     for (int t = 0; t < 3; t++)
         if (n > 8 + t && params[8 + t] >= 0 && params[8 + t] <= 14) h->direct_lg[t] = (int)params[8 + t];
     if (n > 11 && params[11] > 0 && params[11] <= 4) h->load_shift_wide = (int)params[11];
+    if (n > 12 && params[12] >= 0) h->tiny_rows = params[12];   // 0 disables the single-pass path
     return MM_OK;
 }
 

@@ -90,7 +90,7 @@ struct RowFetcher {
                 n = wk.count - b < MM_ROWS_PER_FETCH ? wk.count - b : MM_ROWS_PER_FETCH;
                 q = 0;
                 if (lane < n) {
-                    li = wk.rows[b + lane];
+                    li = wk.rows ? wk.rows[b + lane] : b + lane;   // rows == nullptr: every row in order
                     las = p.a_ptr[li];
                     lae = p.a_ptr[li + 1];
                     lms = p.m_ptr[li];
@@ -110,7 +110,7 @@ struct RowFetcher {
             const int r = *s_row;
             group_bar(bar_id, GW * 32);
             if (r >= wk.count) return false;
-            ri.i = wk.rows[r];
+            ri.i = wk.rows ? wk.rows[r] : r;
             ri.as = p.a_ptr[ri.i];
             ri.ae = p.a_ptr[ri.i + 1];
             ri.ms = p.m_ptr[ri.i];

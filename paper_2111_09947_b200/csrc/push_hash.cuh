@@ -813,9 +813,27 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
     unsigned long long evaluated = 0;
     RowFetcher<GW> rf;
     RowInfo ri;
-    while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
-        hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg[ri.i], cap_lg_max, gt, bar_id,
-                                                s_warp + g * GW, bsm, wq, dummy_s, evaluated);
+    while (rf.next(p, wk, gt, bar_id, s_row + g, ri)) {
+        if (!row_cap_lg) {
+            // small-problem path (no analysis pass before it): every row with
+            // the full table; a plain mask row over half of it is left to the
+            // host's fallback to the binned path
+            if (ri.me - ri.ms > (1 << (cap_lg_max - 1))) {
+                if (gt == 0) {
+                    atomicExch(o.overflow, 1);
+                    o.row_nnz[ri.i] = 0;
+                }
+                continue;
+            }
+            if (ri.ae == ri.as || ri.me == ri.ms) {   // no products / empty mask row
+                if (gt == 0) o.row_nnz[ri.i] = 0;
+                continue;
+            }
+        }
+        hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg ? row_cap_lg[ri.i] : cap_lg_max,
+                                                cap_lg_max, gt, bar_id, s_warp + g * GW, bsm, wq, dummy_s,
+                                                evaluated);
+    }
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);
         if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);
