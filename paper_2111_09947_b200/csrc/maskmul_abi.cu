@@ -1049,6 +1049,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
         if (n > 8 + t && params[8 + t] >= 0 && params[8 + t] <= 14) h->direct_lg[t] = (int)params[8 + t];
     if (n > 11 && params[11] > 0 && params[11] <= 4) h->load_shift_wide = (int)params[11];
     if (n > 12 && params[12] >= 0) h->tiny_rows = params[12];   // 0 disables the single-pass path
+    if (n > 13 && params[13] >= 0) h->tiny_nnz = params[13];
     return MM_OK;
 }
 
