@@ -76,3 +76,29 @@ def test_cfg2_input_pipeline_on_device():
     want = load_json("configs.json")["cfg2"]["digest_m"]   # the pattern of L
     low.values = None
     assert digest_mat(low) == want
+
+
+def test_prep_edge_cases():
+    """Empty edge lists, only self-loops, a single vertex, duplicate-only
+    input, and an empty graph through relabel / tril / transpose."""
+    for n, r, c in ((5, [], []), (4, [0, 1, 2, 3], [0, 1, 2, 3]), (1, [0], [0]), (3, [1, 1, 1], [2, 2, 2])):
+        r = np.asarray(r, dtype=np.int64)
+        c = np.asarray(c, dtype=np.int64)
+        want = simple_undirected_graph(from_arrays(n, n, r, c, np.ones(r.size, dtype=np.int64)))
+        got = prep.simple_undirected_graph(r, c, n)
+        _same(got, want)
+        rl, perm = degree_sort_relabel(want)
+        drl, dperm = prep.degree_sort_relabel(got)
+        assert np.array_equal(dperm.cpu().numpy(), perm)
+        _same(drl, rl)
+        _same(prep.tril_strict(drl), tril_strict(rl))
+        t = got.transpose_storage()
+        assert np.array_equal(t.ptr.cpu().numpy(), to_csc(want).col_ptr)
+    # rectangular transpose with an empty row block and int64 values
+    a = from_arrays(6, 3, np.array([0, 0, 5]), np.array([2, 0, 1]), np.array([7, 8, 9], dtype=np.int64))
+    da = DeviceCsr.from_host(a, dtype=np.int64)
+    t = da.transpose_storage()
+    want = to_csc(a)
+    assert np.array_equal(t.ptr.cpu().numpy(), want.col_ptr)
+    assert np.array_equal(t.idx.cpu().numpy(), want.row_idx[: want.nnz])
+    assert np.array_equal(t.values.cpu().numpy(), want.values[: want.nnz])
