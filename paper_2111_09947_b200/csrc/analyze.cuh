@@ -109,7 +109,9 @@ __host__ __device__ constexpr int64_t msas_bytes(int64_t words, int64_t nm, int 
 }
 // dense window: a state per column of the window plus a guard column
 __host__ __device__ constexpr int64_t msad_bytes(int64_t words, int kind) {
-    return (kind == 0 ? 4 : 12) * (32 * words + 1);
+    // budget accounting: the state (+ value) per window column; the guard
+    // column on top is not charged (a 512-column window fits the 1-warp tier)
+    return (kind == 0 ? 4 : 12) * (32 * words);
 }
 __host__ __device__ constexpr int64_t mca_bytes(int64_t nm, int kind) {
     return (kind == 0 ? 8 : 16) * nm;
@@ -171,7 +173,7 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         return BIN_MSAD0 + (ap.ordered ? tf : tr);
     // complemented MSA / auto with an output narrow enough for a state per column
     if (ap.comp && (ap.family == FAM_MSA || ap.family == FAM_AUTO) &&
-        msad_bytes((ncols + 31) >> 5, kind) - (kind == 0 ? 4 : 12) <= ap.rank_budget[tf]) {   // guard column free
+        msad_bytes((ncols + 31) >> 5, kind) <= ap.rank_budget[tf]) {
         *aux_out = (ncols + 31) >> 5;
         return BIN_MSADC0 + tf;
     }
