@@ -162,6 +162,19 @@ int mm_symbolic(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask,
 int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops, int64_t* total,
                  void* stream);
 
+/* Work estimate per row, w_i = flops_i + nnz(M_i) (the multi-GPU row cuts and
+ * the per-row cost model; SURVEY §8(b) "mm_row_work").  row_flops (optional)
+ * also receives flops_i. */
+int mm_row_work(const mm_matrix_t* a, const mm_matrix_t* b, const mm_matrix_t* mask, int64_t* row_flops,
+                int64_t* row_work, void* stream);
+
+/* Device workspace one multiply draws from the stream-ordered pool (the
+ * library allocates it itself with cudaMallocAsync and returns it at
+ * mm_multiply_end).  Complemented one-phase plans add 12 bytes per bound
+ * slot, sum_i min(flops_i, ncols) (known after mm_row_flops), not included. */
+int mm_workspace_bytes(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+                       const mm_matrix_t* b, size_t* bytes);
+
 /* np.cumsum into a row pointer (multiply.py:366-367,391-392):
  * out[0] = 0, out[i+1] = out[i] + counts[i]; n+1 outputs. */
 int mm_exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, void* stream);

@@ -21,7 +21,8 @@ EXPORTS = ("mm_abi_version", "mm_last_error", "mm_create", "mm_destroy", "mm_mul
            "mm_compact_rows", "mm_reduce_sum", "mm_profile_enable", "mm_profile_read",
            "mm_profile_bins", "mm_set_tuning", "mm_filter_min", "mm_lookup_rows",
            "mm_bc_dependency_weights", "mm_bc_scale_by", "mm_ewise_add_begin", "mm_ewise_add_end",
-           "mm_bc_accumulate", "mm_csr_from_coo", "mm_expand_rows", "mm_degree_order")
+           "mm_bc_accumulate", "mm_csr_from_coo", "mm_expand_rows", "mm_degree_order", "mm_row_work",
+           "mm_workspace_bytes")
 MM_COO_SYMMETRIC, MM_COO_NO_DIAG, MM_COO_LOWER, MM_COO_DEDUP = 1, 2, 4, 8
 
 
@@ -81,6 +82,8 @@ def load(path: str | None = None):
                                     C.POINTER(C.c_int64), P]
     lib.mm_expand_rows.argtypes = [C.c_int64, P, P, P]
     lib.mm_degree_order.argtypes = [PM, P, P, P]
+    lib.mm_row_work.argtypes = [PM, PM, PM, P, P, P]
+    lib.mm_workspace_bytes.argtypes = [C.POINTER(PlanT), PM, PM, PM, C.POINTER(C.c_size_t)]
     for name in EXPORTS:
         getattr(lib, name)
         if name not in ("mm_last_error",):

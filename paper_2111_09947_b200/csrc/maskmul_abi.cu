@@ -1117,6 +1117,46 @@ int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops,
     return MM_OK;
 }
 
+// w_i = flops_i + nnz(M_i): the work estimate behind the multi-GPU cuts and
+// the per-row cost model (SURVEY §8(b) mm_row_work, §8(e)).
+__global__ void k_add_row_lengths(int64_t n, const int64_t* ptr, int64_t* w) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        w[i] += ptr[i + 1] - ptr[i];
+}
+
+int mm_row_work(const mm_matrix_t* a, const mm_matrix_t* b, const mm_matrix_t* mask, int64_t* row_flops,
+                int64_t* row_work, void* stream) {
+    if (!a || !b || !mask || !row_work) return fail(MM_ERR_INPUT, "null argument");
+    if (mask->nrows != a->nrows) return fail(MM_ERR_INPUT, "mask and A row counts differ");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = mm_row_flops(a, b, row_work, nullptr, stream);
+    if (rc) return rc;
+    if (row_flops && a->nrows > 0)
+        CU(cudaMemcpyAsync(row_flops, row_work, a->nrows * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    if (a->nrows > 0) {
+        ++g_launches;
+        k_add_row_lengths<<<(int)std::min<int64_t>((a->nrows + 255) / 256, 148 * 8), 256, 0, st>>>(
+            a->nrows, mask->ptr, row_work);
+        CU(cudaGetLastError());
+    }
+    return MM_OK;
+}
+
+int mm_workspace_bytes(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+                       const mm_matrix_t* b, size_t* bytes) {
+    if (!plan || !mask || !a || !b || !bytes) return fail(MM_ERR_INPUT, "null argument");
+    const int64_t m = mask->nrows;
+    const bool comp = plan->complemented != 0;
+    auto r = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    size_t t = r(sizeof(Summary) + (3 * NBINS + 4) * sizeof(int32_t)) + r(m * 4) /* long rows */ +
+               3 * r(m * 8) + r((m + 1) * 8) + r(scan_scratch_elems(m) * 8) + r(m * 4) + 2 * r(m);
+    if (comp && plan->phases == 1) t += r(m * 8) + r((m + 1) * 8);
+    if (!comp && plan->phases == 1) t += r(mask->nnz * 4) + r(mask->nnz * 8);
+    if (plan->phases == 2) t += r(m * 8);
+    *bytes = t;
+    return MM_OK;
+}
+
 int mm_exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, void* stream) {
     if (!out || (n > 0 && !counts)) return fail(MM_ERR_INPUT, "null argument");
     return exclusive_scan(counts, n, out, (cudaStream_t)stream);

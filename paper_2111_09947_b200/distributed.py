@@ -73,6 +73,21 @@ def concat_row_blocks(parts: list[DeviceCsr]) -> DeviceCsr:
     return DeviceCsr(sum(p.nrows for p in parts), parts[0].ncols, ptr, idx, vals)
 
 
+def row_work_device(a: DeviceCsr, b: DeviceCsr, m: DeviceCsr) -> torch.Tensor:
+    """w_i = flops_i + nnz(M_i) on the device (mm_row_work), the same numbers
+    as ``row_work`` without a host round trip of A."""
+    import ctypes as C
+
+    from . import _lib
+    from .multiply import _raise
+    w = torch.empty(max(a.nrows, 1), dtype=torch.int64, device=a.idx.device)
+    rc = _lib.load().mm_row_work(C.byref(a.mm()), C.byref(b.mm()), C.byref(m.mm()), None, w.data_ptr(),
+                                 C.c_void_p(torch.cuda.current_stream(a.idx.device).cuda_stream))
+    if rc:
+        _raise(rc)
+    return w[: a.nrows]
+
+
 def broadcast_csr(m: DeviceCsr | None, src: int, device, meta_dtype=None) -> DeviceCsr:
     """Replicate a CSR from rank `src` to every rank (NCCL broadcast on GPU,
     gloo on CPU).  Non-source ranks pass m=None."""

@@ -395,3 +395,26 @@ def test_compact_rows_row_search_edges(shape):
     m = int(cnt.sum())
     assert np.array_equal(oi[:m].cpu().numpy(), tmp_idx[keep])
     assert np.array_equal(ov[:m].cpu().numpy(), tmp_val[keep])
+
+
+def test_row_work_and_workspace_estimate():
+    """mm_row_work (w_i = flops_i + nnz(M_i), multiply.py:103-108 + mask
+    lengths) equals the host row_work; mm_workspace_bytes covers the slab."""
+    import ctypes as C
+    from paper_2111_09947_b200 import _lib
+    from paper_2111_09947_b200.distributed import row_work, row_work_device
+    from paper_2111_09947_b200.multiply import _plan_t
+    rng = np.random.default_rng(8)
+    a = random_csr(rng, 3000, 900, 7)
+    b = random_csr(rng, 900, 1200, 9)
+    m = random_csr(rng, 3000, 1200, 5)
+    da, db = DeviceCsr.from_host(a, with_values=False), DeviceCsr.from_host(b, with_values=False)
+    dm = DeviceCsr.from_host(m, with_values=False)
+    got = row_work_device(da, db, dm).cpu().numpy()
+    want = row_work(a.row_ptr, a.col_idx, b.row_ptr, m.row_ptr)
+    assert np.array_equal(got, want)
+    nbytes = C.c_size_t(0)
+    pt = _plan_t(MultiplyPlan(), False)
+    assert _lib.load().mm_workspace_bytes(C.byref(pt), C.byref(dm.mm()), C.byref(da.mm()), C.byref(db.mm()),
+                                          C.byref(nbytes)) == 0
+    assert nbytes.value >= 3000 * 8 * 3 + m.nnz * 12
