@@ -104,13 +104,19 @@ class MultiplyStats:
 # handles
 # ---------------------------------------------------------------------------
 
-_handles: dict[int, int] = {}
+_handles: dict[tuple[int, int], int] = {}
 _lock = threading.Lock()
 
 
 def _handle(device_index: int) -> int:
+    """One library handle per (device, thread): a handle carries the state
+    between mm_multiply_begin and mm_multiply_end, so threads never share one."""
+    key = (device_index, threading.get_ident())
+    h = _handles.get(key)
+    if h is not None:
+        return h
     with _lock:
-        h = _handles.get(device_index)
+        h = _handles.get(key)
         if h is None:
             lib = _lib.load()
             hp = C.c_void_p()
@@ -118,7 +124,7 @@ def _handle(device_index: int) -> int:
             if rc:
                 raise RuntimeError(f"mm_create failed: {_lib.last_error()}")
             h = hp.value
-            _handles[device_index] = h
+            _handles[key] = h
         return h
 
 

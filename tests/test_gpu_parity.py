@@ -418,3 +418,36 @@ def test_row_work_and_workspace_estimate():
     assert _lib.load().mm_workspace_bytes(C.byref(pt), C.byref(dm.mm()), C.byref(da.mm()), C.byref(db.mm()),
                                           C.byref(nbytes)) == 0
     assert nbytes.value >= 3000 * 8 * 3 + m.nnz * 12
+
+
+def test_concurrent_threads_share_no_handle():
+    """Two host threads multiplying at once on one device (each gets its own
+    library handle) produce the same C as a single thread."""
+    import threading
+    w = workloads.cfg1()
+    da = DeviceCsr.from_host(w.a, dtype=np.float64)
+    dm = DeviceCsr.from_host(w.mask, with_values=False)
+    plan = MultiplyPlan(semiring=w.semiring)
+    ref, _ = multiply_device(dm, da, da, plan)
+    torch.cuda.synchronize()
+    out, errs = [], []
+
+    def work():
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(20):
+                    c, _ = multiply_device(dm, da, da, plan, stream=s)
+                s.synchronize()
+                out.append(c)
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append(e)
+
+    ts = [threading.Thread(target=work) for _ in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for c in out:
+        assert torch.equal(c.idx, ref.idx) and torch.equal(c.values, ref.values)
