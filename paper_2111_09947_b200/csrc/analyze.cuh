@@ -33,7 +33,8 @@ enum Bin : int {
     BIN_MSAS0 = 36,   // + tier (0..2): MSA with a sparse two-level window bitmap
     BIN_MSAD0 = 39,   // + tier (0..2): MSA with a dense per-column window (push_dense.cuh)
     BIN_MSADC0 = 42,  // + tier (0..2): complemented MSA over every column (narrow outputs)
-    NBINS = 45
+    BIN_PULL_LANE = 45,  // pull, one lane per mask entry (short masks, short A rows and B columns)
+    NBINS = 46
 };
 __host__ __device__ constexpr bool is_msadc_bin(int b) { return b >= BIN_MSADC0 && b < BIN_MSADC0 + 3; }
 __host__ __device__ constexpr bool is_msas_bin(int b) { return b >= BIN_MSAS0 && b < BIN_MSAS0 + 3; }
@@ -150,7 +151,11 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             else if (tr == 0 && nm <= ap.auto_mca_nm) fam = FAM_MCA;
         }
     }
-    if (fam == FAM_PULL) return BIN_PULL;
+    if (fam == FAM_PULL) {
+        // short masks, A rows and B^T columns: a lane per mask entry runs the merge
+        if (nm <= 32 && na <= 128 && pull_cols <= 32 * nm) return BIN_PULL_LANE;
+        return BIN_PULL;
+    }
     if (fam == FAM_HEAP) {
         // plain: mask-rank slots in shared memory (tier 0) or global (tier 1);
         // complement rows with <= 32 A entries: sorted single-batch merge (2)
@@ -256,7 +261,7 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const bool want_pull = ap.family == FAM_AUTO && ap.has_bt && !ap.comp;
+    const bool want_pull = (ap.family == FAM_AUTO || ap.family == FAM_PULL) && ap.has_bt && !ap.comp;
     unsigned long long my_flops = 0, my_bound = 0;
     for (int64_t r0 = warp * 32; r0 < p.nrows; r0 += nwarps * 32) {
         const int64_t i = r0 + lane;
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(256) k_analyze_long(Prob p, AnalyzeParams ap, 
     __shared__ long long s_red[8];
     const int n_long = *long_rows_n;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const bool want_pull = ap.family == FAM_AUTO && ap.has_bt && !ap.comp;
+    const bool want_pull = (ap.family == FAM_AUTO || ap.family == FAM_PULL) && ap.has_bt && !ap.comp;
     for (int q = blockIdx.x; q < n_long; q += gridDim.x) {
         const int64_t i = long_rows[q];
         const int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1], ms = p.m_ptr[i], me = p.m_ptr[i + 1];

@@ -418,7 +418,24 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
         const int cnt = h->sum.bin_count[b];
         cudaStream_t st = concurrent ? h->aux[oi % mm_handle::NAUX] : main_st;
         Work wk{h->rows_list + h->bin_off[b], cnt, cursors + b};
-        if (b == BIN_PULL) {
+        // a lane per mask entry needs many rows to fill the GPU; small bins
+        // run the warp-per-row kernel (same results)
+        if (b == BIN_PULL_LANE && cnt >= 16384) {
+            const int kind = numeric ? h->kind : 0;
+            void (*kern)(Prob, Out, Work);
+            if (!numeric) kern = k_pull_lane<0, false>;
+            else if (kind == 0) kern = k_pull_lane<0, true>;
+            else if (kind == 1) kern = k_pull_lane<1, true>;
+            else kern = k_pull_lane<2, true>;
+            int occ = 0;
+            if ((rc = kernel_occupancy((const void*)kern, 256, 0, &occ))) return rc;
+            const int grid = std::max(1, std::min((cnt + 255) / 256, std::max(occ, 1) * h->num_sms));
+            ++g_launches;
+            kern<<<grid, 256, 0, st>>>(h->prob, out, wk);
+            CU(cudaGetLastError());
+            continue;
+        }
+        if (b == BIN_PULL || b == BIN_PULL_LANE) {
             int kind = numeric ? h->kind : 0;
             int stage = std::min(std::max(h->sum.max_na, 2), 512);
             stage += stage & 1;
@@ -830,7 +847,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     h->stats = mm_stats_t{};
     h->stats.generated_flops = (int64_t)h->sum.gen_flops;
     h->stats.rows_empty = h->sum.bin_count[BIN_EMPTY];
-    h->stats.rows_pull = h->sum.bin_count[BIN_PULL];
+    h->stats.rows_pull = h->sum.bin_count[BIN_PULL] + h->sum.bin_count[BIN_PULL_LANE];
     h->stats.rows_push = m - h->stats.rows_empty - h->stats.rows_pull;
     mark(h, 2);
 
