@@ -240,10 +240,30 @@ def _prepare(mask, a, b, plan: MultiplyPlan, device=None):
     b_csr = to_csr(b) if is_csc else b
     db = DeviceCsr.from_host(b_csr, dtype=dt, device=device, with_values=need_vals)
     dbt = None
-    if plan.algorithm == "inner" or (plan.algorithm == "auto" and is_csc):
+    if plan.algorithm == "inner" or (plan.algorithm == "auto" and (is_csc or (not comp and _pull_pays(mask, a, b_csr)))):
         dbt = (DeviceCsr.from_host(b, dtype=dt, device=device, with_values=need_vals)
                if is_csc else db.transpose_storage())
     return dm, da, db, dbt, comp
+
+
+def _pull_pays(mask, a, b) -> bool:
+    """auto: build B^T in the (untimed) preparation when the byte model of
+    SURVEY §8(d) makes pull clearly cheaper in aggregate — the mask is much
+    sparser than the product space (cfg3 d1 / d4).  The per-row choice is
+    still made on the device by the analysis kernel."""
+    nnz_a = int(a.row_ptr[-1])
+    nnz_m = int(mask.row_ptr[-1])
+    if nnz_a == 0 or nnz_m == 0:
+        return False
+    blen = np.diff(np.asarray(b.row_ptr, dtype=np.int64))
+    flops = int(blen[np.asarray(a.col_idx[:nnz_a], dtype=np.int64)].sum())
+    # pull reads (nnz(A_i) + nnz(B_*j)) per mask entry (i, j)
+    na = np.diff(np.asarray(a.row_ptr, dtype=np.int64))
+    nm = np.diff(np.asarray(mask.row_ptr, dtype=np.int64))
+    nnz_b = int(b.row_ptr[-1])
+    col_len = np.bincount(np.asarray(b.col_idx[:nnz_b], dtype=np.int64), minlength=b.shape[1])
+    pull = int((na * nm).sum()) + int(col_len[np.asarray(mask.col_idx[:nnz_m], dtype=np.int64)].sum())
+    return 3 * pull < 2 * flops
 
 
 def masked_multiply_with_stats(mask, a, b, plan: MultiplyPlan, device=None):
