@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .build import LIB_PATH
+from .build import LIB_PATH, MMIO_LIB_PATH
 
 MM_ALGO = {"msa": 0, "hash": 1, "mca": 2, "heap": 3, "heapdot": 4, "inner": 5, "auto": 6}
 MM_OK, MM_ERR_PLAN, MM_ERR_INPUT, MM_ERR_INTERNAL, MM_ERR_CUDA = 0, 1, 2, 3, 4
@@ -96,3 +96,37 @@ def load(path: str | None = None):
 def last_error() -> str:
     msg = load().mm_last_error()
     return msg.decode() if msg else ""
+
+
+# every symbol declared in include/maskmul_mmio.h
+MMIO_EXPORTS = ("mmx_read_header", "mmx_read_entries")
+MMX_OK, MMX_ERR_FORMAT, MMX_ERR_OVERFLOW = 0, 2, 5
+MMX_FIELDS = ("real", "integer", "pattern")
+
+
+class MmxHeaderT(C.Structure):
+    _fields_ = [("field", C.c_int32), ("symmetric", C.c_int32), ("nrows", C.c_int64), ("ncols", C.c_int64),
+                ("nnz", C.c_int64), ("data_offset", C.c_int64), ("data_line", C.c_int64)]
+
+
+_mmio = None
+
+
+def load_mmio(path: str | None = None):
+    """Load the host Matrix Market reader (no Python fallback parser)."""
+    global _mmio
+    if _mmio is not None:
+        return _mmio
+    path = path or MMIO_LIB_PATH
+    if not os.path.exists(path):
+        raise RuntimeError(f"Matrix Market reader missing at {path}: run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    P = C.c_void_p
+    lib.mmx_read_header.argtypes = [P, C.c_int64, C.POINTER(MmxHeaderT), C.POINTER(C.c_int64), C.c_char_p,
+                                    C.c_int]
+    lib.mmx_read_entries.argtypes = [P, C.c_int64, C.POINTER(MmxHeaderT), P, P, P, C.c_int,
+                                     C.POINTER(C.c_int64), C.c_char_p, C.c_int]
+    for name in MMIO_EXPORTS:
+        getattr(lib, name).restype = C.c_int
+    _mmio = lib
+    return lib

@@ -10,6 +10,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(OUT_DIR, "libmaskmul_b200.so")
+# host-only Matrix Market reader (include/maskmul_mmio.h): loads without a GPU
+MMIO_LIB_PATH = os.path.join(OUT_DIR, "libmaskmul_mmio.so")
+MMIO_SOURCE = "mmio_host.cpp"
 SOURCES = ["maskmul_abi.cu"]
 HEADERS = ["common.cuh", "analyze.cuh", "product_loop.cuh", "push_hash.cuh", "push_rank.cuh", "push_heap.cuh", "push_single.cuh", "push_msa_sparse.cuh", "push_dense.cuh",
            "pull_inner.cuh", "scan_compact.cuh", "graph_ops.cuh"]
@@ -37,7 +40,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def build_mmio(force: bool = False, verbose: bool = False) -> str:
+    src = os.path.join(CSRC, MMIO_SOURCE)
+    hdr = os.path.join(os.path.dirname(HERE), "include", "maskmul_mmio.h")
+    if (not force and os.path.exists(MMIO_LIB_PATH)
+            and os.path.getmtime(MMIO_LIB_PATH) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
+        return MMIO_LIB_PATH
+    os.makedirs(OUT_DIR, exist_ok=True)
+    tmp = MMIO_LIB_PATH + ".tmp"
+    cmd = [shutil.which("g++") or "g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-pthread",
+           "-Wall", "-Wextra", "-o", tmp, src]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, MMIO_LIB_PATH)
+    return MMIO_LIB_PATH
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_mmio(force=force, verbose=verbose)
     if not force and not _stale():
         return LIB_PATH
     os.makedirs(OUT_DIR, exist_ok=True)

@@ -102,3 +102,39 @@ def test_prep_edge_cases():
     assert np.array_equal(t.ptr.cpu().numpy(), want.col_ptr)
     assert np.array_equal(t.idx.cpu().numpy(), want.row_idx[: want.nnz])
     assert np.array_equal(t.values.cpu().numpy(), want.values[: want.nnz])
+
+
+@pytest.mark.parametrize("field,symmetric,dups", [("pattern", True, True), ("pattern", False, False),
+                                                  ("real", False, False), ("real", True, False),
+                                                  ("integer", False, True)])
+def test_matrix_market_device_matches_host(tmp_path, field, symmetric, dups):
+    """mmio.read_matrix_market_device == the host reader (which matches the
+    reference bitwise, tests/test_mmio.py), for the canonical CSR and values."""
+    from paper_2111_09947_b200.mmio import read_matrix_market, read_matrix_market_device
+    rng = np.random.default_rng(31 + len(field) + symmetric)
+    n, nnz = 20000, 150000
+    key = rng.choice(n * n, nnz, replace=dups)
+    r, c = key // n, key % n
+    if symmetric:
+        r, c = np.maximum(r, c), np.minimum(r, c)
+        if not dups:   # keep the lower triangle free of repeats after folding
+            k2 = np.unique(r * n + c)
+            r, c = k2 // n, k2 % n
+    lines = [f"%%MatrixMarket matrix coordinate {field} {'symmetric' if symmetric else 'general'}\n",
+             f"{n} {n} {r.size}\n"]
+    vals = rng.standard_normal(r.size)
+    for t in range(r.size):
+        v = "" if field == "pattern" else f" {float(vals[t])!r}" if field == "real" else f" {t % 17 - 8}"
+        lines.append(f"{r[t] + 1} {c[t] + 1}{v}\n")
+    p = tmp_path / "g.mtx"
+    p.write_text("".join(lines))
+    host = read_matrix_market(p)
+    dev = read_matrix_market_device(p, device="cuda:0")
+    _same(dev, host)
+    if field == "pattern":
+        assert dev.values is None
+        full = read_matrix_market_device(p, device="cuda:0", with_values=True)
+        _same(full, host)
+        assert np.array_equal(full.values.cpu().numpy(), host.values)
+    else:
+        assert np.array_equal(dev.values.cpu().numpy(), host.values)   # bitwise (fp64 sums in file order)
