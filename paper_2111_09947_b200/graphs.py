@@ -20,7 +20,7 @@ import numpy as np
 from .device import DeviceCsr
 from .multiply import MultiplyPlan, PlanError, multiply_device, reduce_sum
 from .semiring import arithmetic_semiring, plus_pair_semiring
-from .sparse import CsrMatrix, SparseError, is_pattern_symmetric
+from .sparse import CsrMatrix, SparseError
 
 
 @dataclass(frozen=True)
@@ -48,25 +48,35 @@ class KernelResult:
     per_multiply: list = field(default_factory=list)
 
 
-def _check_simple_symmetric(g: CsrMatrix, what: str) -> None:
+def _simple_symmetric_on_device(g: CsrMatrix, what: str, device) -> DeviceCsr:
+    """Upload the pattern and run graphs.py:75-84's checks on the device: square,
+    pattern-symmetric (equal to its own canonical transpose, built by
+    prep.transpose as is_pattern_symmetric does on the host, sparse.py:294-300),
+    no self-loops.  Same errors as the reference; the host transpose of a
+    scale-22 graph took longer than the whole k-truss on the device."""
+    import torch
+
+    from . import prep
     if g.nrows != g.ncols:
         raise SparseError(f"{what} requires a square adjacency matrix")
-    if not is_pattern_symmetric(g):
+    dg = DeviceCsr.from_host(g, device=device, with_values=False)
+    t = prep.transpose(dg)
+    if not (torch.equal(t.ptr, dg.ptr) and torch.equal(t.idx, dg.idx)):
         raise SparseError(f"{what} requires a pattern-symmetric adjacency matrix; "
                           "normalize with simple_undirected_graph() first")
-    rows, cols, _ = g.triples()
-    if np.any(rows == cols):
+    if dg.nnz and bool((prep.expand_rows(dg) == dg.idx).any()):
         raise SparseError(f"{what} requires a simple graph (no self-loops); "
                           "normalize with simple_undirected_graph() first")
+    return dg
 
 
 def triangle_count(g: CsrMatrix, plan: MultiplyPlan, device=None) -> KernelResult:
     """graphs.py:87-96.  The relabel + strict lower triangle run on the device
     (prep.triangle_lower, identical to the host tril_strict(degree_sort_relabel))."""
     from . import prep
-    _check_simple_symmetric(g, "triangle counting")
+    dg = _simple_symmetric_on_device(g, "triangle counting", device)
     kplan = replace(plan, semiring=plus_pair_semiring(np.int64), complemented=False)
-    dl = prep.triangle_lower(DeviceCsr.from_host(g, device=device, with_values=False))
+    dl = prep.triangle_lower(dg)
     c, st = multiply_device(dl, dl, dl, kplan,
                             b_csc=dl.transpose_storage() if kplan.algorithm == "inner" else None)
     total = int(reduce_sum(c.values).item()) if c.nnz else 0
@@ -90,10 +100,9 @@ def k_truss(g: CsrMatrix, k: int, plan: MultiplyPlan, device=None) -> KernelResu
 
     if k < 3:
         raise ValueError("k-truss needs k >= 3")
-    _check_simple_symmetric(g, "k-truss")
+    cur = _simple_symmetric_on_device(g, "k-truss", device)
     kplan = replace(plan, semiring=plus_pair_semiring(np.int64), complemented=False)
     res = KernelResult(None)
-    cur = DeviceCsr.from_host(g, device=device, with_values=False)
     lib = _lib.load()
     while cur.nnz:
         sup, st = multiply_device(cur, cur, cur, kplan,

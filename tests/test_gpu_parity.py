@@ -338,6 +338,17 @@ def test_triangle_count_and_k_truss_graph_kernels():
     assert triangle_count(g, plan).value == k["tc_er10_d8_seed42"]
     assert k_truss(complete(5), 5, plan).value.nnz == 20      # test_graphs.py:72-74
     assert k_truss(complete(4), 5, plan).value.nnz == 0
+    # input checks (graphs.py:75-84, test_graphs.py:55-61), now on the device
+    directed = from_triples(3, 3, [(0, 1, 1), (1, 2, 1), (2, 0, 1)])
+    loop = from_triples(2, 2, [(0, 0, 1), (0, 1, 1), (1, 0, 1)])
+    rect = from_triples(2, 3, [(0, 1, 1)])
+    empty = from_triples(4, 4, [])
+    for fn in (lambda g: triangle_count(g, plan), lambda g: k_truss(g, 3, plan)):
+        for bad in (directed, loop, rect):
+            with pytest.raises(SparseError):
+                fn(bad)
+    assert triangle_count(empty, plan).value == 0
+    assert k_truss(empty, 3, plan).value.nnz == 0
     # R-MAT scale-8 graphs against a host fixed point built on the oracle
     for seed in range(8):
         g = simple_undirected_graph(generate(GeneratorSpec("rmat", 8, 4, seed=seed)))
