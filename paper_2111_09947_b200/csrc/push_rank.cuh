@@ -86,18 +86,35 @@ struct MsaPacked {
 };
 
 // --- MCA rank search -------------------------------------------------------
+template <bool SMEM>
 struct McaRow {
-    const int32_t* m;   // mask row (shared)
+    const int32_t* m;   // mask row (shared when SMEM, else the group's global slab)
     int nm;
     int steps;          // ceil(log2(nm + 1))
+    uint32_t m_s;       // 32-bit shared address of m (SMEM)
+    __device__ __forceinline__ McaRow(const int32_t* m_, int nm_, int steps_) : m(m_), nm(nm_), steps(steps_) {
+        m_s = SMEM ? (uint32_t)__cvta_generic_to_shared(m_) : 0u;
+    }
+    __device__ __forceinline__ int32_t at(int r) const {
+        if (SMEM) {
+            int32_t v;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(m_s + 4u * (uint32_t)r));
+            return v;
+        }
+        return m[r];
+    }
     __device__ __forceinline__ int rank(int32_t j) const {
-        // branch-free lower bound with a fixed step count
+        // branch-free lower bound with a fixed step count: every probe index
+        // is clamped into the row (the select discards out-of-range probes)
+        if (nm == 0) return -1;
         int pos = 0;
         for (int st = steps - 1; st >= 0; st--) {
             const int q = pos + (1 << st);
-            if (q <= nm && m[q - 1] < j) pos = q;
+            const int32_t v = at(min(q, nm) - 1);
+            pos = (q <= nm && v < j) ? q : pos;
         }
-        return (pos < nm && m[pos] == j) ? pos : -1;
+        const int32_t v = at(min(pos, nm - 1));
+        return (pos < nm && v == j) ? pos : -1;
     }
 };
 
@@ -330,12 +347,12 @@ __device__ __forceinline__ void rank_row(const Prob& p, const Out& o, unsigned c
     } else {
         int steps = 0;
         while ((1 << steps) <= nm) steps++;
-        McaRow rb{mrow, nm, steps};
+        McaRow<SMEM> rb(mrow, nm, steps);
         if (KIND == 2) {
-            RankLocatorF64<McaRow> loc{rb, sl.cnt, (double*)sl.val};
+            RankLocatorF64<McaRow<SMEM>> loc{rb, sl.cnt, (double*)sl.val};
             if (!idle) evaluated += ordered_products_f64<NUMERIC>(p, loc, as, ae, lane, c_lo, c_hi);
         } else {
-            RankProber<KIND, NUMERIC, McaRow> pr{rb, sl, p.b_val, 0u};
+            RankProber<KIND, NUMERIC, McaRow<SMEM>> pr{rb, sl, p.b_val, 0u};
             flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm);
             evaluated += pr.evaluated;
         }
