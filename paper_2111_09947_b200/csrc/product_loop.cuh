@@ -179,10 +179,21 @@ __device__ __forceinline__ void tail_chunk(const Prob& p, PR& pr, const int32_t*
 //   product (the policy may use warp collectives).
 //   [c_lo, c_hi): only products with a column in this range (a sub-range of
 //   each sorted B row, by binary search); the default is every product.
-template <int GW, int KIND, class PR>
+//
+//   SEARCH (plain masks): an A entry whose B row is much longer than the
+//   mask part [srch_m, srch_m + srch_nm) makes nm·log2(len) probes instead
+//   of len — each mask column is binary-searched in B_k, and only the columns
+//   found are handed to pr (the same products the scan would keep: the
+//   evaluated set, counts and sums are unchanged).  R-MAT hubs: a 10^5-entry
+//   B row meets mask rows of a few hundred columns (cfg5).
+#ifndef MM_SEARCH_RATIO
+#define MM_SEARCH_RATIO 4
+#endif
+template <int GW, int KIND, class PR, bool SEARCH = false>
 __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as, int64_t ae, int gt,
                                               int bar_id, int* s_warp, BatchSmem bsm,
-                                              int32_t c_lo = INT32_MIN, int32_t c_hi = INT32_MAX) {
+                                              int32_t c_lo = INT32_MIN, int32_t c_hi = INT32_MAX,
+                                              const int32_t* srch_m = nullptr, int64_t srch_nm = 0) {
     constexpr int GT = GW * 32;
 #ifndef MM_PRODUCT_UNROLL
 #define MM_PRODUCT_UNROLL 4
@@ -204,13 +215,19 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
             len = (int)(end - base);
             if (KIND == 1) av = ((const long long*)p.a_val)[t];
         }
+        bool srch = false;
+        if (SEARCH && len > 0) {
+            const int lg = 32 - __clz(len);          // ceil(log2(len + 1))
+            srch = (long long)len > srch_nm * lg * MM_SEARCH_RATIO;
+        }
+        const int flen = srch ? 0 : len;             // scanned products of this entry
         int tot;
-        const int incl = group_incl_scan<GW>(len, &tot, s_warp, bar_id, gt);
+        const int incl = group_incl_scan<GW>(flen, &tot, s_warp, bar_id, gt);
         int q_lo = 0, q_hi = tot;
         int l_lo = 0, l_end = NB;
         if (GW > 1) {
             bsm.incl[gt] = incl;
-            bsm.base[gt] = base - (incl - len);
+            bsm.base[gt] = base - (incl - flen);
             if (KIND == 1) bsm.av[gt] = av;
             group_bar(bar_id, GT);
             const int wg = gt >> 5;
@@ -235,7 +252,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
             int plen = 0;
             if (GW == 1) {
                 sb = base;
-                plen = len;
+                plen = flen;
                 sa = av;
             } else if (l < l_end) {
                 const int e_in = bsm.incl[l];
@@ -334,6 +351,47 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
         }
         pr.drain();
         if (GW > 1) group_bar(bar_id, GT);
+        if (SEARCH) {
+            int ntot;
+            const int sincl = group_incl_scan<GW>(srch ? 1 : 0, &ntot, s_warp, bar_id, gt);
+            if (ntot > 0) {                           // group-uniform
+                if (srch) {
+                    bsm.base[sincl - 1] = base;
+                    bsm.incl[sincl - 1] = len;
+                    if (KIND == 1) bsm.av[sincl - 1] = av;
+                }
+                if (GW > 1) group_bar(bar_id, GT); else __syncwarp();
+                const long long total = (long long)ntot * srch_nm;
+                for (long long w0 = 0; w0 < total; w0 += GT) {
+                    const long long idx = w0 + gt;
+                    int32_t jj[1] = {EMPTY_KEY};
+                    long long aa[1] = {0}, ss[1] = {0};
+                    if (idx < total) {
+                        const int item = (int)(idx / srch_nm);
+                        const int32_t j = srch_m[idx - (long long)item * srch_nm];
+                        const long long b0 = bsm.base[item];
+                        long long lo = b0, cnt = bsm.incl[item];
+                        while (cnt > 0) {                 // lower bound of j in B_k
+                            const long long half = cnt >> 1;
+                            if (__ldg(p.b_idx + lo + half) < j) {
+                                lo += half + 1;
+                                cnt -= half + 1;
+                            } else {
+                                cnt = half;
+                            }
+                        }
+                        if (lo < b0 + bsm.incl[item] && __ldg(p.b_idx + lo) == j) {
+                            jj[0] = j;
+                            ss[0] = lo;
+                            if (KIND == 1) aa[0] = bsm.av[item];
+                        }
+                    }
+                    pr.template put_batch<1>(jj, aa, ss);
+                }
+                pr.drain();
+                if (GW > 1) group_bar(bar_id, GT); else __syncwarp();
+            }
+        }
     }
 }
 

@@ -437,6 +437,9 @@ struct HashLocatorF64 {
 // One part of a row: the mask entries [ms, me) and the products whose column
 // lies in [c_lo, c_hi) (the whole row unless the row is sliced, see
 // hash_row).  Writes its results at w_base (NUMERIC) and returns their count.
+#ifndef MM_SEARCH_ON
+#define MM_SEARCH_ON 1   // mask-driven binary search of long B rows (plain hash rows)
+#endif
 template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
                                          int64_t ms, int64_t me, int32_t c_lo, int32_t c_hi, int64_t w_base,
@@ -576,7 +579,8 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.dummy_s = dummy_s;
         pr.b_val = p.b_val;
         pr.evaluated = 0;
-        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
+        flat_products<GW, KIND, decltype(pr), MODE == MODE_PLAIN && MM_SEARCH_ON>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi,
+                                                                               p.m_idx + ms, nm);
         evaluated += pr.evaluated;
     } else if (CLEAN && pl.hm == 2) {
         DirectProber<KIND, NUMERIC, 2> pr;
@@ -590,7 +594,8 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.dummy_s = dummy_s;
         pr.b_val = p.b_val;
         pr.evaluated = 0;
-        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
+        flat_products<GW, KIND, decltype(pr), MODE == MODE_PLAIN && MM_SEARCH_ON>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi,
+                                                                               p.m_idx + ms, nm);
         evaluated += pr.evaluated;
     } else {
         WarpProber<KIND, MODE, NUMERIC, SMEM> pr;
@@ -608,7 +613,8 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.qn = 0;
         pr.lane = lane;
         pr.evaluated = 0;
-        flat_products<GW, KIND>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi);
+        flat_products<GW, KIND, decltype(pr), MODE == MODE_PLAIN && MM_SEARCH_ON>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi,
+                                                                               p.m_idx + ms, nm);
         evaluated += pr.evaluated;
     }
     group_bar(bar_id, GT);
