@@ -189,6 +189,9 @@ __device__ __forceinline__ void tail_chunk(const Prob& p, PR& pr, const int32_t*
 #ifndef MM_SEARCH_RATIO
 #define MM_SEARCH_RATIO 4
 #endif
+#ifndef MM_SEARCH_U
+#define MM_SEARCH_U 2
+#endif
 template <int GW, int KIND, class PR, bool SEARCH = false>
 __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as, int64_t ae, int gt,
                                               int bar_id, int* s_warp, BatchSmem bsm,
@@ -361,32 +364,57 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                     if (KIND == 1) bsm.av[sincl - 1] = av;
                 }
                 if (GW > 1) group_bar(bar_id, GT); else __syncwarp();
+                // SU interleaved branch-free lower bounds per lane: their
+                // dependent load chains overlap
+                constexpr int SU = MM_SEARCH_U;
                 const long long total = (long long)ntot * srch_nm;
-                for (long long w0 = 0; w0 < total; w0 += GT) {
-                    const long long idx = w0 + gt;
-                    int32_t jj[1] = {EMPTY_KEY};
-                    long long aa[1] = {0}, ss[1] = {0};
-                    if (idx < total) {
-                        const int item = (int)(idx / srch_nm);
-                        const int32_t j = srch_m[idx - (long long)item * srch_nm];
-                        const long long b0 = bsm.base[item];
-                        long long lo = b0, cnt = bsm.incl[item];
-                        while (cnt > 0) {                 // lower bound of j in B_k
-                            const long long half = cnt >> 1;
-                            if (__ldg(p.b_idx + lo + half) < j) {
-                                lo += half + 1;
-                                cnt -= half + 1;
-                            } else {
-                                cnt = half;
-                            }
-                        }
-                        if (lo < b0 + bsm.incl[item] && __ldg(p.b_idx + lo) == j) {
-                            jj[0] = j;
-                            ss[0] = lo;
-                            if (KIND == 1) aa[0] = bsm.av[item];
+                for (long long w0 = 0; w0 < total; w0 += (long long)GT * SU) {
+                    int32_t jj[SU];
+                    long long aa[SU], ss[SU];
+                    const int32_t* bb[SU];
+                    int nn[SU];
+#pragma unroll
+                    for (int u = 0; u < SU; u++) {
+                        const long long idx = w0 + (long long)u * GT + gt;
+                        jj[u] = EMPTY_KEY;
+                        aa[u] = 0;
+                        ss[u] = 0;
+                        bb[u] = p.b_idx;
+                        nn[u] = 0;
+                        if (idx < total) {
+                            const int item = (int)(idx / srch_nm);
+                            jj[u] = srch_m[idx - (long long)item * srch_nm];
+                            ss[u] = bsm.base[item];
+                            bb[u] = p.b_idx + ss[u];
+                            nn[u] = bsm.incl[item];
+                            if (KIND == 1) aa[u] = bsm.av[item];
                         }
                     }
-                    pr.template put_batch<1>(jj, aa, ss);
+                    const int32_t* b0[SU];
+#pragma unroll
+                    for (int u = 0; u < SU; u++) b0[u] = bb[u];
+                    bool more = true;
+                    while (more) {
+                        more = false;
+#pragma unroll
+                        for (int u = 0; u < SU; u++) {
+                            if (nn[u] > 1) {
+                                const int half = nn[u] >> 1;
+                                // last entry <= j (the B row is strictly increasing)
+                                bb[u] = __ldg(bb[u] + half) <= jj[u] ? bb[u] + half : bb[u];
+                                nn[u] -= half;
+                                more |= nn[u] > 1;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < SU; u++) {
+                        // nn == 1: bb = the last entry <= j (or the first entry); nn == 0: no product
+                        const bool hit = nn[u] == 1 && __ldg(bb[u]) == jj[u];
+                        ss[u] += bb[u] - b0[u];
+                        if (!hit) jj[u] = EMPTY_KEY;
+                    }
+                    pr.template put_batch<SU>(jj, aa, ss);
                 }
                 pr.drain();
                 if (GW > 1) group_bar(bar_id, GT); else __syncwarp();
