@@ -211,6 +211,52 @@ def test_narrow_outputs_and_heavy_rows(n):
                     assert st.evaluated_multiplies == r.evaluated_multiplies
 
 
+@pytest.mark.parametrize("tier_rows", [(64, 6), (16, 80), (4, 1500), (2, 7000)])
+def test_search_mode_long_b_rows(tier_rows):
+    """Hub B rows far longer than the mask rows: the plain hash rows
+    binary-search each mask column in B_k instead of scanning it
+    (flat_products SEARCH, product_loop.cuh); the result, the evaluated count
+    and 1P == 2P must not change.  Hub rows of 20K-60K entries, masks of a
+    few to thousands of columns (1-warp, 4-warp, 16-warp and sliced rows),
+    some hub rows repeated inside one A row's batch, plus short B rows
+    mixed in so scan and search share a row."""
+    rows, dm = tier_rows
+    rng = np.random.default_rng(900 + dm)
+    n = 200_000
+    hubs = 12
+    hub_rows = [np.sort(rng.choice(n, int(rng.integers(20_000, 60_000)), replace=False)) for _ in range(hubs)]
+    short = random_csr(rng, 400, n, 5)
+    b_rows = np.concatenate([np.full(h.size, q) for q, h in enumerate(hub_rows)] +
+                            [np.repeat(np.arange(400), np.diff(short.row_ptr)) + hubs])
+    b_cols = np.concatenate(hub_rows + [short.col_idx[: short.nnz]])
+    b = from_arrays(hubs + 400, n, b_rows, b_cols, rng.integers(-5, 6, b_cols.size))
+    a_r, a_c = [], []
+    for i in range(rows):
+        ks = np.unique(np.concatenate([rng.choice(hubs, 3, replace=False), hubs + rng.choice(400, 20)]))
+        a_r.append(np.full(ks.size, i))
+        a_c.append(ks)
+    a = from_arrays(rows, hubs + 400, np.concatenate(a_r), np.concatenate(a_c),
+                    rng.integers(-3, 4, sum(x.size for x in a_c)))
+    # mask columns: half drawn from hub rows (hits), half anywhere
+    m_r, m_c = [], []
+    for i in range(rows):
+        pool = hub_rows[int(rng.integers(hubs))]
+        cols = np.unique(np.concatenate([rng.choice(pool, dm // 2 + 1), rng.choice(n, dm // 2 + 1)]))
+        m_r.append(np.full(cols.size, i))
+        m_c.append(cols)
+    m = from_arrays(rows, n, np.concatenate(m_r), np.concatenate(m_c), np.ones(sum(x.size for x in m_c), np.int64))
+    for sem in (SR, plus_pair_semiring(np.int64)):
+        r = oracle.masked_multiply(m.pattern(), a, b, semiring_id=sem.kernel_id, dtype=sem.dtype)
+        want = digest_csr(r.row_ptr, r.col_idx, r.values)
+        for algo in ("hash", "auto"):
+            for ph in ("1p", "2p"):
+                plan = MultiplyPlan(algorithm=algo, phases=ph, semiring=sem)
+                c, st = masked_multiply_with_stats(m.pattern(), a, b, plan)
+                assert _digest(c) == want, (rows, dm, algo, ph, sem.name)
+                assert st.evaluated_multiplies == r.evaluated_multiplies
+                assert st.generated_flops == r.generated_flops
+
+
 def test_determinism_repeat_and_row_partition():
     w = workloads.cfg1()
     d = [DeviceCsr.from_host(x, dtype=np.float64) for x in (w.a,)]
