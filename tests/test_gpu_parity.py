@@ -211,20 +211,22 @@ def test_narrow_outputs_and_heavy_rows(n):
                     assert st.evaluated_multiplies == r.evaluated_multiplies
 
 
-@pytest.mark.parametrize("tier_rows", [(64, 6), (16, 80), (4, 1500), (2, 7000)])
-def test_search_mode_long_b_rows(tier_rows):
+@pytest.mark.parametrize("spec", [(64, 6, 20_000, 60_000, 200_000), (16, 80, 20_000, 60_000, 200_000),
+                                  (4, 400, 30_000, 60_000, 200_000), (2, 7000, 20_000, 60_000, 200_000),
+                                  (2, 7000, 600_000, 1_000_000, 4_000_000)])
+def test_search_mode_long_b_rows(spec):
     """Hub B rows far longer than the mask rows: the plain hash rows
     binary-search each mask column in B_k instead of scanning it
     (flat_products SEARCH, product_loop.cuh); the result, the evaluated count
     and 1P == 2P must not change.  Hub rows of 20K-60K entries, masks of a
-    few to thousands of columns (1-warp, 4-warp, 16-warp and sliced rows),
+    few to thousands of columns (1-warp, 4-warp, 16-warp and sliced rows; the
+    last case searches inside the column slices of sliced rows),
     some hub rows repeated inside one A row's batch, plus short B rows
     mixed in so scan and search share a row."""
-    rows, dm = tier_rows
-    rng = np.random.default_rng(900 + dm)
-    n = 200_000
+    rows, dm, h_lo, h_hi, n = spec
+    rng = np.random.default_rng(900 + dm + h_lo)
     hubs = 12
-    hub_rows = [np.sort(rng.choice(n, int(rng.integers(20_000, 60_000)), replace=False)) for _ in range(hubs)]
+    hub_rows = [np.sort(rng.choice(n, int(rng.integers(h_lo, h_hi)), replace=False)) for _ in range(hubs)]
     short = random_csr(rng, 400, n, 5)
     b_rows = np.concatenate([np.full(h.size, q) for q, h in enumerate(hub_rows)] +
                             [np.repeat(np.arange(400), np.diff(short.row_ptr)) + hubs])
