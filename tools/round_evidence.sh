@@ -12,3 +12,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_p
   python tools/profile_step.py --reps 1 > gpurun_out/ncu_full_raw.csv 2> gpurun_out/ncu_full.err; echo ncu_full rc=$?
 timeout 1200 python tools/bench_configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err; echo configs rc=$?
 timeout 600 python tools/bench_bc.py --cpu > gpurun_out/bench_bc.json 2> gpurun_out/bench_bc.err; echo bc rc=$?
+timeout 900 python tools/bench_ktruss.py --scale 18 --cpu > gpurun_out/ktruss_s18.json 2> gpurun_out/ktruss_s18.err; echo k18 rc=$?
+timeout 900 python tools/bench_ktruss.py --scale 22 > gpurun_out/ktruss_s22.json 2> gpurun_out/ktruss_s22.err; echo k22 rc=$?
