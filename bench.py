@@ -178,7 +178,7 @@ def run_reference(args, rank):
     import oracle
     oracle.load()
     low, _ = build_inputs(args.scale)
-    workers = oracle.max_threads()
+    workers = oracle.use_all_cores()
     # bound the run to a few minutes: sample a row block if the full multiply is slow
     t0 = time.perf_counter()
     r = cpu_reference_run(low, workers)
@@ -234,10 +234,17 @@ def run_ours(args, rank, world, local_rank):
                                                    row_block, row_work)
     from paper_2111_09947_b200.multiply import _handle, multiply_device, reduce_sum
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; MM_DIST_BACKEND=gloo (with fewer GPUs than ranks)
+    # only exercises the multi-rank plumbing — it is never a measurement
+    backend = os.environ.get("MM_DIST_BACKEND", "nccl")
+    gpu = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
     low, t_gen = build_inputs(args.scale, on_device=True)
     m = low.nrows
@@ -262,7 +269,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     lib = _lib.load()
     import ctypes as C
-    h = _handle(local_rank)
+    h = _handle(gpu)
     lib.mm_profile_enable(h, 1)
 
     def step(a, b, btt):
@@ -283,7 +290,7 @@ def run_ours(args, rank, world, local_rank):
     launches = C.c_int64(0)
     phase = [0.0] * 6
     step_ms = []
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(gpu)
     n_launch_total = 0
     if world > 1:
         dist.barrier()
@@ -367,7 +374,7 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
-        workers = oracle.max_threads()
+        workers = oracle.use_all_cores()
         r = cpu_reference_run(low, workers)
         t1 = time.perf_counter()
         r = cpu_reference_run(low, workers)
@@ -378,12 +385,20 @@ def run_ours(args, rank, world, local_rank):
                          "kernels), best of 2"}
         del t1
 
+    numeric_ms_max = per[2]
+    if world > 1:
+        # per-GPU roofline: the whole job's bytes split over N GPUs, against the
+        # slowest rank's numeric phase (every rank joins this reduction)
+        t = torch.tensor([numeric_ms_max], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        numeric_ms_max = float(t.item())
+
     if rank == 0:
         peak, peak_src = measured_peak()
         nnz_a = low.nnz
         bytes_alg = push_bytes(m, nnz_a, flops, nnz_a, nnz_c, 0)
-        numeric_ms = per[2]
-        achieved = bytes_alg / (numeric_ms * 1e-3) / 1e9
+        numeric_ms = numeric_ms_max
+        achieved = bytes_alg / world / (numeric_ms * 1e-3) / 1e9
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tfile):
@@ -420,7 +435,8 @@ def run_ours(args, rank, world, local_rank):
                          "kernel": "numeric phase: every row-bin kernel of one multiply (MSA bitmap / hash / pull tiers)",
                          "bytes_alg_per_launch": bytes_alg, "kernel_ms": numeric_ms,
                          "peak_source": peak_src,
-                         "step_frac": bytes_alg / (ms_max * 1e-3) / 1e9 / peak},
+                         "per_gpu": world > 1,
+                         "step_frac": bytes_alg / world / (ms_max * 1e-3) / 1e9 / peak},
             "phase_ms": {"analyze": per[0], "scatter": per[1], "numeric": per[2],
                          "scan_readback": per[3], "compact": per[4], "multiply_total": per[5]},
             "bins": bins,

@@ -52,12 +52,22 @@ def load():
     lib.or_symbolic_phase.argtypes = [C.c_int, C.c_int, I64, I64, I64, P, P, P, P, P, P, P,
                                       C.c_int, P]
     lib.or_max_threads.restype = C.c_int
+    lib.or_set_threads.argtypes = [C.c_int]
+    lib.or_set_threads.restype = None
     _lib = lib
     return lib
 
 
 def max_threads() -> int:
     return int(load().or_max_threads())
+
+
+def use_all_cores() -> int:
+    """Run later oracle calls on every core this process may use (torchrun
+    sets OMP_NUM_THREADS=1 per rank); returns the thread count."""
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    load().or_set_threads(n)
+    return max_threads()
 
 
 @dataclass
