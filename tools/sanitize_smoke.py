@@ -53,6 +53,22 @@ c = masked_multiply(m.pattern(), a, b, MultiplyPlan(algorithm="hash", semiring=p
 assert np.array_equal(c.col_idx, r.col_idx) and np.array_equal(c.values, r.values)
 checks += 1
 
+# search mode: hub B rows far longer than the mask rows (1-warp / 4-warp / 16-warp hash rows)
+from paper_2111_09947_b200.sparse import from_arrays as _fa
+for rows_s, dm_s in ((16, 3), (4, 40), (2, 300)):
+    hubs = [np.sort(rng.choice(40000, int(rng.integers(3000, 9000)), replace=False)) for _ in range(6)]
+    b_r = np.concatenate([np.full(h.size, q) for q, h in enumerate(hubs)])
+    b_s = _fa(6, 40000, b_r, np.concatenate(hubs), rng.integers(-4, 5, b_r.size))
+    a_s = _fa(rows_s, 6, np.repeat(np.arange(rows_s), 6), np.tile(np.arange(6), rows_s), rng.integers(-3, 4, rows_s * 6))
+    mr = np.repeat(np.arange(rows_s), dm_s)
+    mc = np.concatenate([rng.choice(hubs[i % 6], dm_s) for i in range(rows_s)])
+    m_s = _fa(rows_s, 40000, mr, mc, np.ones(mr.size, dtype=np.int64))
+    for sem in (arithmetic_semiring(np.int64), plus_pair_semiring(np.int64)):
+        r = oracle.masked_multiply(m_s.pattern(), a_s, b_s, semiring_id=sem.kernel_id, dtype=sem.dtype)
+        c = masked_multiply(m_s.pattern(), a_s, b_s, MultiplyPlan(algorithm="hash", semiring=sem))
+        assert np.array_equal(c.col_idx, r.col_idx) and np.array_equal(c.values, r.values)
+        checks += 1
+
 # graph drivers and device input preparation
 import torch
 from paper_2111_09947_b200 import prep
