@@ -187,7 +187,10 @@ __device__ __forceinline__ void tail_chunk(const Prob& p, PR& pr, const int32_t*
 //   evaluated set, counts and sums are unchanged).  R-MAT hubs: a 10^5-entry
 //   B row meets mask rows of a few hundred columns (cfg5).
 #ifndef MM_SEARCH_RATIO
-#define MM_SEARCH_RATIO 4
+#define MM_SEARCH_RATIO 1   // search when len > RATIO/DEN * nm * ceil(log2(len + 1))
+#endif
+#ifndef MM_SEARCH_DEN
+#define MM_SEARCH_DEN 1
 #endif
 #ifndef MM_SEARCH_U
 #define MM_SEARCH_U 2
@@ -221,7 +224,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
         bool srch = false;
         if (SEARCH && len > 0) {
             const int lg = 32 - __clz(len);          // ceil(log2(len + 1))
-            srch = (long long)len > srch_nm * lg * MM_SEARCH_RATIO;
+            srch = (long long)len * MM_SEARCH_DEN > srch_nm * lg * MM_SEARCH_RATIO;
         }
         const int flen = srch ? 0 : len;             // scanned products of this entry
         int tot;
