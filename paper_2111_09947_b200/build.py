@@ -14,8 +14,12 @@ LIB_PATH = os.path.join(OUT_DIR, "libmaskmul_b200.so")
 MMIO_LIB_PATH = os.path.join(OUT_DIR, "libmaskmul_mmio.so")
 MMIO_SOURCE = "mmio_host.cpp"
 SOURCES = ["maskmul_abi.cu"]
-HEADERS = ["common.cuh", "analyze.cuh", "product_loop.cuh", "push_hash.cuh", "push_rank.cuh", "push_heap.cuh", "push_single.cuh", "push_msa_sparse.cuh", "push_dense.cuh",
-           "pull_inner.cuh", "scan_compact.cuh", "graph_ops.cuh"]
+
+
+def headers() -> list[str]:
+    """Every csrc/*.cuh (globbed, so a new header can never be missed by _stale)."""
+    return sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
+
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -35,7 +39,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB_PATH):
         return True
     t = os.path.getmtime(LIB_PATH)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + headers()]
     deps.append(os.path.join(os.path.dirname(HERE), "include", "maskmul_b200.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 

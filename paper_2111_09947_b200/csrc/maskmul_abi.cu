@@ -108,6 +108,45 @@ int read_i64s(const void* dptr, int64_t* out, int n, cudaStream_t st) {
 
 int read_i64(const void* dptr, int64_t* out, cudaStream_t st) { return read_i64s(dptr, out, 1, st); }
 
+// Scoped device selection for every extern "C" entry: the call runs on the
+// device that owns its handle / stream / operands and the caller's current
+// device is restored on return (torch keeps its own notion of the current
+// device, which the library must not change behind its back).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        int cur = -1;
+        if (dev < 0 || cudaGetDevice(&cur) != cudaSuccess || cur == dev) return;
+        if (cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Device of a device pointer (-1 when it is not device memory / unknown).
+int pointer_device(const void* ptr) {
+    if (!ptr) return -1;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged ? at.device : -1;
+}
+
+// Device a free-standing call runs on: the stream's device for a created
+// stream, else the device holding its first operand (the legacy default
+// stream belongs to whichever device is current).
+int call_device(void* stream, const void* operand) {
+    int d = -1;
+    if (stream && cudaStreamGetDevice((cudaStream_t)stream, &d) == cudaSuccess) return d;
+    cudaGetLastError();
+    return pointer_device(operand);
+}
+
 }  // namespace
 
 struct mm_handle {
@@ -257,6 +296,12 @@ int validate(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* 
                                       std::to_string(b->nrows) + ", " + std::to_string(b->ncols) + ")");
     if (a->nrows < 0 || a->nrows >= (1ll << 31) || b->ncols >= (1ll << 31) || a->ncols >= (1ll << 31))
         return fail(MM_ERR_INPUT, "dimensions must be < 2^31");
+    // The product loops count one batch of A entries' products (distinct
+    // rows of B, canonical A) in 32-bit ints: nnz(B) < 2^31 bounds every such
+    // sum (product_loop.cuh flat_products / ordered_products_f64).
+    if (a->nnz < 0 || b->nnz < 0 || mask->nnz < 0 || b->nnz >= (1ll << 31) || a->nnz >= (1ll << 31) ||
+        mask->nnz >= (1ll << 31))
+        return fail(MM_ERR_INPUT, "nnz of A, B and the mask must be in [0, 2^31)");
     if ((a->nnz && (!a->ptr || !a->idx)) || !a->ptr || !b->ptr || !mask->ptr)
         return fail(MM_ERR_INPUT, "missing index arrays");
     if (plan->semiring == MM_SR_ARITHMETIC && ((a->nnz && !a->values) || (b->nnz && !b->values)))
@@ -275,28 +320,38 @@ int validate(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* 
 // shared-memory attribute and the occupancy query are host API calls worth a
 // few microseconds each, so results are cached per (kernel, threads, smem).
 struct OccEntry {
+    int device;
     const void* fn;
     int threads;
     size_t smem;
     int occ;
 };
 thread_local std::vector<OccEntry> g_occ_cache;
-thread_local std::vector<std::pair<const void*, size_t>> g_smem_attr;
+struct SmemAttr {
+    int device;
+    const void* fn;
+    size_t bytes;
+};
+thread_local std::vector<SmemAttr> g_smem_attr;
 
+// Keyed by device as well: cudaFuncSetAttribute applies to the current
+// device's context only, so a thread that multiplies on two GPUs sets it on each.
 int kernel_occupancy(const void* fn, int threads, size_t smem, int* occ) {
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
     for (const OccEntry& e : g_occ_cache)
-        if (e.fn == fn && e.threads == threads && e.smem == smem) { *occ = e.occ; return MM_OK; }
+        if (e.device == dev && e.fn == fn && e.threads == threads && e.smem == smem) { *occ = e.occ; return MM_OK; }
     size_t* have = nullptr;
     for (auto& a : g_smem_attr)
-        if (a.first == fn) have = &a.second;
-    if (!have) { g_smem_attr.push_back({fn, 0}); have = &g_smem_attr.back().second; }
+        if (a.device == dev && a.fn == fn) have = &a.bytes;
+    if (!have) { g_smem_attr.push_back({dev, fn, 0}); have = &g_smem_attr.back().bytes; }
     if (smem > *have) {
         CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         *have = smem;
     }
     int o = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
-    g_occ_cache.push_back({fn, threads, smem, o});
+    g_occ_cache.push_back({dev, fn, threads, smem, o});
     *occ = o;
     return MM_OK;
 }
@@ -666,7 +721,6 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     int rc = validate(plan, mask, a, b, bt);
     if (rc) return rc;
     if (h->active) release(h);
-    CU(cudaSetDevice(h->device));
     h->stream = st;
     h->launch_base = g_launches;
     mark(h, 0);
@@ -979,10 +1033,13 @@ const char* mm_last_error(void) { return g_last_error.c_str(); }
 
 int mm_create(int device, mm_handle_t** out) {
     if (!out) return fail(MM_ERR_INPUT, "null handle pointer");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return fail(MM_ERR_CUDA, cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(MM_ERR_INPUT, "no CUDA device " + std::to_string(device));
+    DeviceGuard dg(device);
     mm_handle* h = new mm_handle();
     h->device = device;
-    cudaError_t e = cudaSetDevice(device);
-    if (e != cudaSuccess) { delete h; return fail(MM_ERR_CUDA, cudaGetErrorString(e)); }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -1000,6 +1057,7 @@ int mm_create(int device, mm_handle_t** out) {
 
 int mm_destroy(mm_handle_t* h) {
     if (!h) return MM_OK;
+    DeviceGuard dg(h->device);
     if (h->active) release(h);
     if (h->stream) cudaStreamSynchronize(h->stream);
     cudaFreeHost(h->h_summary);
@@ -1019,6 +1077,7 @@ int mm_destroy(mm_handle_t* h) {
 int mm_multiply_begin(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
                       const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* out_nnz) {
     if (!h || !out_nnz) return fail(MM_ERR_INPUT, "null argument");
+    DeviceGuard dg(h->device);
     int rc = begin_impl(h, plan, mask, a, b, b_csc, (cudaStream_t)stream, false, nullptr, out_nnz);
     if (rc) release(h);
     return rc;
@@ -1026,11 +1085,13 @@ int mm_multiply_begin(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* 
 
 int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_values, mm_stats_t* stats) {
     if (!h) return fail(MM_ERR_INPUT, "null handle");
+    DeviceGuard dg(h->device);
     return end_impl(h, c_row_ptr, c_col_idx, c_values, stats);
 }
 
 int mm_profile_enable(mm_handle_t* h, int on) {
     if (!h) return fail(MM_ERR_INPUT, "null handle");
+    DeviceGuard dg(h->device);
     if (on && !h->ev[0]) {
         for (auto& e : h->ev) CU(cudaEventCreate(&e));
     }
@@ -1042,6 +1103,7 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches) {
     if (!h) return fail(MM_ERR_INPUT, "null handle");
     if (launches) *launches = h->launches;
     if (!h->prof || !ms) return MM_OK;
+    DeviceGuard dg(h->device);
     CU(cudaEventSynchronize(h->ev[5]));
     static const int from[6] = {0, 1, 2, 3, 4, 0};
     static const int to[6] = {1, 2, 3, 4, 5, 5};
@@ -1082,6 +1144,7 @@ int mm_profile_bins(mm_handle_t* h, int64_t* rows, int64_t* flops, int n) {
 int mm_symbolic(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
                 const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* counts) {
     if (!h || !counts) return fail(MM_ERR_INPUT, "null argument");
+    DeviceGuard dg(h->device);
     cudaStream_t st = (cudaStream_t)stream;
     if (mask && mask->nrows > 0) {
         cudaError_t e = cudaMemsetAsync(counts, 0, mask->nrows * sizeof(int64_t), st);
@@ -1100,6 +1163,7 @@ int mm_symbolic(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, 
 int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops, int64_t* total, void* stream) {
     if (!a || !b || !row_flops) return fail(MM_ERR_INPUT, "null argument");
     if (a->ncols != b->nrows) return fail(MM_ERR_INPUT, "dimension mismatch");
+    DeviceGuard dg(call_device(stream, a->ptr));
     cudaStream_t st = (cudaStream_t)stream;
     Prob p{};
     p.a_ptr = a->ptr; p.a_idx = a->idx; p.b_ptr = b->ptr; p.b_idx = b->idx;
@@ -1145,6 +1209,7 @@ int mm_row_work(const mm_matrix_t* a, const mm_matrix_t* b, const mm_matrix_t* m
                 int64_t* row_work, void* stream) {
     if (!a || !b || !mask || !row_work) return fail(MM_ERR_INPUT, "null argument");
     if (mask->nrows != a->nrows) return fail(MM_ERR_INPUT, "mask and A row counts differ");
+    DeviceGuard dg(call_device(stream, a->ptr));
     cudaStream_t st = (cudaStream_t)stream;
     int rc = mm_row_flops(a, b, row_work, nullptr, stream);
     if (rc) return rc;
@@ -1176,6 +1241,7 @@ int mm_workspace_bytes(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_
 
 int mm_exclusive_scan(const int64_t* counts, int64_t n, int64_t* out, void* stream) {
     if (!out || (n > 0 && !counts)) return fail(MM_ERR_INPUT, "null argument");
+    DeviceGuard dg(call_device(stream, out));
     return exclusive_scan(counts, n, out, (cudaStream_t)stream);
 }
 
@@ -1183,6 +1249,7 @@ int mm_compact_rows(int64_t nrows, const int64_t* bounds_off, const int64_t* row
                     const void* tmp_val, const int64_t* out_ptr, int32_t* out_idx, void* out_val, int dtype,
                     void* stream) {
     if (nrows <= 0) return MM_OK;
+    DeviceGuard dg(call_device(stream, out_ptr));
     cudaStream_t st = (cudaStream_t)stream;
     int* flag = nullptr;
     CU(cudaMallocAsync((void**)&flag, sizeof(int), st));
@@ -1208,6 +1275,7 @@ int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32
                   int64_t* out_nnz, void* stream) {
     if (!c || !out_row_ptr || !out_nnz) return fail(MM_ERR_INPUT, "null argument");
     if (c->nnz > 0 && (!c->values || !c->idx || !out_idx)) return fail(MM_ERR_INPUT, "values and output indices required");
+    DeviceGuard dg(call_device(stream, out_row_ptr));
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t m = c->nrows;
     int64_t* counts = nullptr;
@@ -1237,6 +1305,7 @@ int mm_filter_min(const mm_matrix_t* c, int64_t thr, int64_t* out_row_ptr, int32
 
 int mm_reduce_sum(const void* values, int64_t n, int dtype, void* out, void* stream) {
     if (!out) return fail(MM_ERR_INPUT, "null argument");
+    DeviceGuard dg(call_device(stream, out));
     cudaStream_t st = (cudaStream_t)stream;
     const int nparts = 592;
     void* partials = nullptr;
@@ -1269,6 +1338,7 @@ int mm_lookup_rows(const mm_matrix_t* x, const mm_matrix_t* y, int dtype, void* 
     if (x->nrows != y->nrows || x->ncols != y->ncols) return fail(MM_ERR_INPUT, "lookup_rows: shape mismatch");
     if (x->nnz == 0 || x->nrows == 0) return MM_OK;
     if (y->nnz > 0 && !y->values) return fail(MM_ERR_INPUT, "lookup_rows: Y needs values");
+    DeviceGuard dg(call_device(stream, x->ptr));
     cudaStream_t st = (cudaStream_t)stream;
     ++g_launches;
     if (dtype == MM_DTYPE_FLOAT64)
@@ -1289,6 +1359,7 @@ int mm_bc_dependency_weights(const mm_matrix_t* sigma, const mm_matrix_t* delta,
     if (sigma->nrows != delta->nrows || sigma->nrows != paths->nrows)
         return fail(MM_ERR_INPUT, "bc weights: row count mismatch");
     if (sigma->nnz == 0) return MM_OK;
+    DeviceGuard dg(call_device(stream, sigma->ptr));
     ++g_launches;
     k_lookup<LK_BC_WEIGHT, double><<<warp_grid(sigma->nrows), 256, 0, (cudaStream_t)stream>>>(
         sigma->nrows, sigma->ptr, sigma->idx, nullptr, delta->ptr, delta->idx, (const double*)delta->values,
@@ -1301,6 +1372,7 @@ int mm_bc_scale_by(const mm_matrix_t* x, const mm_matrix_t* paths, double* out, 
     if (!x || !paths || (x->nnz > 0 && (!out || !x->values))) return fail(MM_ERR_INPUT, "null argument");
     if (x->nrows != paths->nrows) return fail(MM_ERR_INPUT, "bc scale: row count mismatch");
     if (x->nnz == 0) return MM_OK;
+    DeviceGuard dg(call_device(stream, x->ptr));
     ++g_launches;
     k_lookup<LK_SCALE, double><<<warp_grid(x->nrows), 256, 0, (cudaStream_t)stream>>>(
         x->nrows, x->ptr, x->idx, (const double*)x->values, paths->ptr, paths->idx, (const double*)paths->values,
@@ -1314,6 +1386,7 @@ int mm_ewise_add_begin(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* c_ro
     if (a->nrows != b->nrows || a->ncols != b->ncols)
         return fail(MM_ERR_INPUT, "shape mismatch (" + std::to_string(a->nrows) + ", " + std::to_string(a->ncols) +
                                       ") vs (" + std::to_string(b->nrows) + ", " + std::to_string(b->ncols) + ")");
+    DeviceGuard dg(call_device(stream, c_row_ptr));
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t m = a->nrows;
     int64_t* counts = nullptr;
@@ -1338,6 +1411,7 @@ int mm_ewise_add_end(const mm_matrix_t* a, const mm_matrix_t* b, int dtype, cons
     if ((a->nnz || b->nnz) && (!c_idx || !c_val)) return fail(MM_ERR_INPUT, "output arrays required");
     const int64_t m = a->nrows;
     if (m == 0 || (a->nnz == 0 && b->nnz == 0)) return MM_OK;
+    DeviceGuard dg(call_device(stream, c_row_ptr));
     cudaStream_t st = (cudaStream_t)stream;
     ++g_launches;
     if (dtype == MM_DTYPE_FLOAT64)
@@ -1356,6 +1430,7 @@ int mm_bc_accumulate(const mm_matrix_t* delta, const int32_t* src_col, double* s
     if (!delta || !scores || (delta->nnz > 0 && !delta->values)) return fail(MM_ERR_INPUT, "null argument");
     const int64_t m = delta->nrows;
     if (m == 0) return MM_OK;
+    DeviceGuard dg(call_device(stream, scores));
     ++g_launches;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)148 * 16));
     k_bc_accumulate<<<grid, 256, 0, (cudaStream_t)stream>>>(m, delta->ptr, delta->idx, (const double*)delta->values,
@@ -1369,6 +1444,7 @@ int mm_bc_accumulate(const mm_matrix_t* delta, const int32_t* src_col, double* s
 int mm_expand_rows(int64_t nrows, const int64_t* ptr, int32_t* rows, void* stream) {
     if (nrows <= 0) return MM_OK;
     if (!ptr || !rows) return fail(MM_ERR_INPUT, "null argument");
+    DeviceGuard dg(call_device(stream, rows));
     ++g_launches;
     k_expand_rows<<<warp_grid(nrows), 256, 0, (cudaStream_t)stream>>>(nrows, ptr, rows);
     CU(cudaGetLastError());
@@ -1431,6 +1507,7 @@ int mm_csr_from_coo(int64_t nrows, int64_t ncols, const void* rows, const void* 
     const bool dedup = flags & MM_COO_DEDUP;
     if ((flags & MM_COO_SYMMETRIC) && nrows != ncols) return fail(MM_ERR_INPUT, "symmetrising needs a square matrix");
     if (dedup && vals) return fail(MM_ERR_INPUT, "duplicate merging is pattern-only");
+    DeviceGuard dg(call_device(stream, out_ptr));
     cudaStream_t st = (cudaStream_t)stream;
     CooView v{rows, cols, idx64, map, (flags & MM_COO_SYMMETRIC) ? 1 : 0, (flags & MM_COO_NO_DIAG) ? 1 : 0,
               (flags & MM_COO_LOWER) ? 1 : 0, nnz};
@@ -1484,6 +1561,7 @@ int mm_degree_order(const mm_matrix_t* g, int32_t* perm, int32_t* new_label, voi
     if (g->nrows != g->ncols) return fail(MM_ERR_INPUT, "degree_sort_relabel requires a square matrix");
     const int64_t n = g->nrows;
     if (n == 0) return MM_OK;
+    DeviceGuard dg(call_device(stream, perm));
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long* mx = nullptr;
     CU(cudaMallocAsync((void**)&mx, sizeof(unsigned long long), st));

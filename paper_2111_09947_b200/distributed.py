@@ -5,7 +5,11 @@ M_i and the referenced B rows only: multiply.py:8-11), so the multi-GPU form
 is a row-block partition:
 
 * A and M are cut into contiguous row blocks of balanced masked work
-  (w_i = flops_i + nnz(M_i), prefix-sum cuts — ``balanced_cuts``);
+  (w_i = flops_i + nnz(M_i), prefix-sum cuts — ``balanced_cuts``), then
+  re-balanced by the kernels' measured cost: each block's weights are scaled
+  by its measured time over its predicted work and the cuts recomputed
+  (``refine_cuts``; bench.py does this during warm-up, since search-mode and
+  sliced hub rows cost far less / more than their flops);
 * B is replicated: rank 0 broadcasts it once over NCCL (NVLink/NVSwitch);
 * each rank multiplies its block with no data-path collective;
 * C row blocks concatenate (``concat_row_blocks`` / ``gather_to_rank0``),
@@ -26,8 +30,9 @@ from .device import DeviceCsr
 
 def balanced_cuts(work: np.ndarray, parts: int) -> np.ndarray:
     """Row cut points [0, c1, ..., nrows] splitting sum(work) into `parts`
-    contiguous blocks of (nearly) equal weight."""
-    work = np.asarray(work, dtype=np.int64)
+    contiguous blocks of (nearly) equal weight (integer or float weights)."""
+    work = np.asarray(work)
+    work = work.astype(np.float64 if work.dtype.kind == "f" else np.int64, copy=False)
     n = work.shape[0]
     if parts <= 1 or n == 0:
         return np.array([0, n], dtype=np.int64)
@@ -41,6 +46,27 @@ def balanced_cuts(work: np.ndarray, parts: int) -> np.ndarray:
     return np.maximum.accumulate(cuts)
 
 
+def refine_cuts(work: np.ndarray, cuts, block_cost, parts: int | None = None) -> np.ndarray:
+    """Cost-aware re-cut: scale the weights of every block [cuts[r],
+    cuts[r+1]) by block_cost[r] / sum(work in block) — the measured cost per
+    unit of predicted work, piecewise constant per block — and recompute the
+    balanced cuts.  Blocks with no predicted work keep their weights."""
+    w = np.asarray(work, dtype=np.float64).copy()
+    cuts = np.asarray(cuts, dtype=np.int64)
+    for r in range(len(cuts) - 1):
+        lo, hi = int(cuts[r]), int(cuts[r + 1])
+        tot = w[lo:hi].sum()
+        if hi > lo and tot > 0:
+            w[lo:hi] *= float(block_cost[r]) / tot
+    return balanced_cuts(w, parts or len(cuts) - 1)
+
+
+def imbalance(block_cost) -> float:
+    """max / mean of per-block costs (1.0 = perfect balance)."""
+    c = np.asarray(block_cost, dtype=np.float64)
+    return float(c.max() / c.mean()) if c.size and c.mean() > 0 else 1.0
+
+
 def row_work(a_row_ptr: np.ndarray, a_col_idx: np.ndarray, b_row_ptr: np.ndarray,
              m_row_ptr: np.ndarray) -> np.ndarray:
     """w_i = flops_i + nnz(M_i) (host numpy; flops_per_row of multiply.py:103-108)."""
@@ -52,13 +78,29 @@ def row_work(a_row_ptr: np.ndarray, a_col_idx: np.ndarray, b_row_ptr: np.ndarray
     return flops + np.diff(m_row_ptr)
 
 
-def row_block(m: DeviceCsr, lo: int, hi: int) -> DeviceCsr:
-    """Rows [lo, hi) of a device CSR as a standalone CSR (views + rebased ptr)."""
-    p0 = int(m.ptr[lo].item())
-    p1 = int(m.ptr[hi].item())
+def row_block(m: DeviceCsr, lo: int, hi: int, p0: int | None = None, p1: int | None = None) -> DeviceCsr:
+    """Rows [lo, hi) of a device CSR as a standalone CSR (views + rebased ptr).
+    p0 / p1 = ptr[lo] / ptr[hi] when the caller already knows them (no host
+    sync); else they are read back."""
+    if p0 is None or p1 is None:
+        p0, p1 = (int(x) for x in m.ptr[torch.tensor([lo, hi], device=m.ptr.device)].tolist())
     ptr = m.ptr[lo: hi + 1] - p0
     vals = m.values[p0:p1] if m.values is not None else None
     return DeviceCsr(hi - lo, m.ncols, ptr.contiguous(), m.idx[p0:p1], vals)
+
+
+def cut_offsets(m: DeviceCsr, cuts) -> list[int]:
+    """ptr[c] for every cut c, in one device->host read."""
+    idx = torch.as_tensor(np.asarray(cuts, dtype=np.int64), device=m.ptr.device)
+    return [int(x) for x in m.ptr[idx].tolist()]
+
+
+def row_blocks(m: DeviceCsr, cuts, offsets: list[int] | None = None) -> list[DeviceCsr]:
+    """Every row block [cuts[r], cuts[r+1]) of m (one host read for all of
+    them, none when the offsets are given)."""
+    offsets = cut_offsets(m, cuts) if offsets is None else offsets
+    return [row_block(m, int(cuts[r]), int(cuts[r + 1]), offsets[r], offsets[r + 1])
+            for r in range(len(cuts) - 1)]
 
 
 def concat_row_blocks(parts: list[DeviceCsr]) -> DeviceCsr:

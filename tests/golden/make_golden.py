@@ -10,6 +10,7 @@ fixtures that the oracle and the CUDA path are pinned against.
     ... make_golden.py --cfg2                          # R-MAT s20 triangle count (~1 min)
     ... make_golden.py --cfg5                          # R-MAT s22 k-truss support (~8 min)
     ... make_golden.py --bc                            # betweenness centrality scores
+    ... make_golden.py --acceptance                    # the reference's acceptance properties
 
 Digest convention (shared with tests/golden_util.py): sha256 over the
 little-endian bytes of int64 row_ptr, then int64 col_idx[:nnz], then the values
@@ -355,12 +356,121 @@ def make_bc():
     return out
 
 
+# ---------------------------------------------------------------------------
+# the reference's own acceptance properties, frozen for the GPU path
+# ---------------------------------------------------------------------------
+
+def acceptance_instance(rng):
+    """pkg/tests/test_acceptance.py:41-49 (_random_instance), same draw order."""
+    n = int(rng.integers(8, 129))
+    d_in = int(rng.integers(1, 17))
+    d_mask = int(rng.integers(1, 17))
+    a = random_csr(rng, n, n, d_in)
+    b = random_csr(rng, n, n, d_in)
+    m = random_csr(rng, n, n, d_mask)
+    comp = bool(rng.integers(0, 2))
+    return n, a, b, m, comp
+
+
+def make_acceptance():
+    """C1 (test_acceptance.py:78-98: 500 instances, seed 5001, every plan incl.
+    heap NInspect 0/1/inf, exact vs the dense oracle), C10 (:248-272:
+    complement duality, seed 110, 100 instances, msa/hash/heap), the full-mask
+    and CSC-B properties of test_multiply.py (:59-65, :169-186, rng fixture
+    seed 20240811) and a signed-zero KAT (_kernels.py:59: the first product is
+    stored, not added to +0.0).  Every expected output is the reference's own,
+    and C1's is also checked here against the reference's dense oracle."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from oracles import dense_masked_product
+    from maskmul.sparse import to_csc
+    sr = arithmetic_semiring(np.int64)
+    out = {}
+    rng = np.random.default_rng(5001)
+    c1 = []
+    for _ in range(500):
+        n, a, b, m, comp = acceptance_instance(rng)
+        keep, values = dense_masked_product(m.to_dense() != 0, a.to_dense(), b.to_dense(), comp)
+        rows, cols = np.nonzero(keep)
+        want = from_arrays(a.nrows, b.ncols, rows, cols, values[rows, cols])
+        sig = None
+        for plan in all_plans(comp, sr) + [MultiplyPlan(algorithm="heap", phases=ph, complemented=comp,
+                                                        semiring=sr, n_inspect=math.inf)
+                                           for ph in ("1p", "2p")]:
+            c, st = masked_multiply_with_stats(m.pattern(), a, b, plan)
+            assert c.equals(want), plan.label()
+            s2 = (digest_csr(c.row_ptr, c.col_idx, c.values), st.generated_flops, st.evaluated_multiplies)
+            assert sig is None or s2 == sig
+            sig = s2
+        c1.append({"n": n, "complemented": comp, "digest_c": sig[0], "generated": sig[1],
+                   "evaluated": sig[2], "nnz": want.nnz, "digest_a": digest_mat(a), "digest_m": digest_mat(m)})
+    out["c1"] = {"seed": 5001, "instances": c1}
+    rng = np.random.default_rng(110)
+    c10 = []
+    for _ in range(100):
+        n = int(rng.integers(8, 65))
+        a = random_csr(rng, n, n, 4)
+        b = random_csr(rng, n, n, 4)
+        m = random_csr(rng, n, n, 4)
+        rec = {"n": n}
+        for algo in ("msa", "hash", "heap"):
+            plain = masked_multiply_with_stats(m.pattern(), a, b, MultiplyPlan(algorithm=algo, semiring=sr))[0]
+            comp = masked_multiply_with_stats(m.pattern(complemented=True), a, b,
+                                              MultiplyPlan(algorithm=algo, semiring=sr))[0]
+            whole = masked_multiply_with_stats(MaskView.full(n, n), a, b,
+                                               MultiplyPlan(algorithm=algo, semiring=sr))[0]
+            assert plain.nnz + comp.nnz == whole.nnz
+            d = {k: digest_csr(x.row_ptr, x.col_idx, x.values)
+                 for k, x in (("plain", plain), ("comp", comp), ("whole", whole))}
+            assert rec.get("digests", d) == d
+            rec["digests"] = d
+        c10.append(rec)
+    out["c10"] = {"seed": 110, "instances": c10}
+    rng = np.random.default_rng(20240811)          # the reference's rng fixture
+    a = random_csr(rng, 32, 32, 4)
+    b = random_csr(rng, 32, 32, 4)
+    whole = masked_multiply_with_stats(MaskView.full(32, 32), a, b, MultiplyPlan(semiring=sr))[0]
+    dense = a.to_dense() @ b.to_dense()
+    assert np.array_equal(whole.to_dense(), dense)
+    out["full_mask"] = {"seed": 20240811, "digest_c": digest_csr(whole.row_ptr, whole.col_idx, whole.values),
+                        "dense_sum": int(dense.sum())}
+    rng = np.random.default_rng(20240811)
+    a = random_csr(rng, 12, 12, 3)
+    b = random_csr(rng, 12, 12, 3)
+    mask = random_csr(rng, 12, 12, 3).pattern()
+    want = masked_multiply_with_stats(mask, a, b, MultiplyPlan(semiring=sr))[0]
+    csc = {}
+    for algo in ("msa", "hash", "mca", "heap", "heapdot", "inner"):
+        c = masked_multiply_with_stats(mask, a, to_csc(b), MultiplyPlan(algorithm=algo, semiring=sr))[0]
+        assert c.equals(want), algo
+        csc[algo] = digest_csr(c.row_ptr, c.col_idx, c.values)
+    out["csc_b"] = {"seed": 20240811, "digest_c": digest_csr(want.row_ptr, want.col_idx, want.values),
+                    "per_algorithm": csc}
+    # signed zero: (-1.0) * 0.0 = -0.0 is stored as the slot's first product;
+    # a second product -0.0 keeps it -0.0; +0.0 + (-0.0) would give +0.0
+    f64 = arithmetic_semiring(np.float64)
+    a = from_triples(2, 2, [(0, 0, -1.0), (1, 0, -1.0), (1, 1, 2.0)]).astype(np.float64)
+    b = from_triples(2, 2, [(0, 0, 0.0), (0, 1, 3.0), (1, 0, -0.0)]).astype(np.float64)
+    a.values[:] = [-1.0, -1.0, 2.0]
+    b.values[:] = [0.0, 3.0, -0.0]
+    kat = {}
+    for plan in all_plans(False, f64):
+        c = masked_multiply_with_stats(MaskView.full(2, 2), a, b, plan)[0]
+        kat[plan.label() + ("" if plan.n_inspect is None else f"-ni{plan.n_inspect}")] = {
+            "cols": c.col_idx.tolist(), "vals_hex": [float(x).hex() for x in c.values]}
+    out["signed_zero"] = {"a": [[0, 0, "-0x1.0000000000000p+0"], [1, 0, "-0x1.0000000000000p+0"],
+                                [1, 1, "0x1.0000000000000p+1"]],
+                          "b": [[0, 0, "0x0.0p+0"], [0, 1, "0x1.8000000000000p+1"], [1, 0, "-0x0.0p+0"]],
+                          "per_plan": kat}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
     ap.add_argument("--cfg5", action="store_true")
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--bc", action="store_true")
+    ap.add_argument("--acceptance", action="store_true")
     args = ap.parse_args()
     meta = {"numpy": np.__version__, "reference": "maskmul " + maskmul.__version__,
             "python": sys.version.split()[0]}
@@ -383,6 +493,9 @@ def main():
     if args.bc:
         with open(os.path.join(HERE, "bc.json"), "w") as f:
             json.dump({"meta": meta, "cases": make_bc()}, f)
+    if args.acceptance:
+        with open(os.path.join(HERE, "acceptance.json"), "w") as f:
+            json.dump({"meta": meta, **make_acceptance()}, f)
     if args.cfg2:
         cfgs["cfg2"] = cfg2()
     if args.cfg5:

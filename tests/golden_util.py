@@ -89,3 +89,16 @@ def regenerate_random_cases():
         else:
             sem = arithmetic_semiring(np.int64)
         yield case, a, b, mm, sem
+
+
+def acceptance_instance(rng):
+    """The reference's acceptance instance (pkg/tests/test_acceptance.py:41-49),
+    restated with the same draw order as make_golden.acceptance_instance."""
+    n = int(rng.integers(8, 129))
+    d_in = int(rng.integers(1, 17))
+    d_mask = int(rng.integers(1, 17))
+    a = random_csr(rng, n, n, d_in)
+    b = random_csr(rng, n, n, d_in)
+    m = random_csr(rng, n, n, d_mask)
+    comp = bool(rng.integers(0, 2))
+    return n, a, b, m, comp

@@ -143,3 +143,37 @@ def test_bc_oracle_matches_reference_scores_bitwise():
                 assert np.array_equal(got.view(np.int64), ref.view(np.int64)), (spec["graph"], algo)
             n_checked += 1
     assert n_checked >= 15
+
+
+def test_acceptance_fixtures_oracle():
+    """The oracle against the reference's acceptance fixtures (acceptance.json:
+    C1 seed-5001 sweep and C10 complement duality, test_acceptance.py:78-98,
+    248-272; signed-zero KAT, _kernels.py:59)."""
+    from golden_util import acceptance_instance, random_csr
+    fx = load_json("acceptance.json")
+    rng = np.random.default_rng(fx["c1"]["seed"])
+    for rec in fx["c1"]["instances"]:
+        n, a, b, m, comp = acceptance_instance(rng)
+        assert digest_mat(a) == rec["digest_a"] and digest_mat(m) == rec["digest_m"]
+        algos = ["msa", "hash", "heap"] + ([] if comp else ["mca", "inner"])
+        for algo in algos:
+            r = oracle.masked_multiply(m.pattern(), a, b, algorithm=algo, complemented=comp)
+            assert digest_csr(r.row_ptr, r.col_idx, r.values) == rec["digest_c"], algo
+            assert (r.generated_flops, r.evaluated_multiplies) == (rec["generated"], rec["evaluated"])
+    rng = np.random.default_rng(fx["c10"]["seed"])
+    for rec in fx["c10"]["instances"]:
+        n = int(rng.integers(8, 65))
+        a, b, m = (random_csr(rng, n, n, 4) for _ in range(3))
+        got = {}
+        for key, mask, comp in (("plain", m.pattern(), False), ("comp", m.pattern(), True),
+                                ("whole", MaskView.full(n, n), False)):
+            r = oracle.masked_multiply(mask, a, b, algorithm="msa", complemented=comp)
+            got[key] = digest_csr(r.row_ptr, r.col_idx, r.values)
+        assert got == rec["digests"]
+    kat = fx["signed_zero"]
+    from paper_2111_09947_b200.sparse import from_arrays
+    a = from_arrays(2, 2, [0, 1, 1], [0, 0, 1], np.array([float.fromhex(v) for _, _, v in kat["a"]]))
+    b = from_arrays(2, 2, [0, 0, 1], [0, 1, 0], np.array([float.fromhex(v) for _, _, v in kat["b"]]))
+    for algo in ("msa", "hash", "mca", "inner"):
+        r = oracle.masked_multiply(MaskView.full(2, 2), a, b, algorithm=algo, dtype=np.float64)
+        assert [float(x).hex() for x in r.values] == kat["per_plan"]["MSA-1P"]["vals_hex"], algo
