@@ -16,9 +16,12 @@ device->host read of the triangle count inside the timed region.
     python bench.py [--gpus N --steps K --warmup W]       # ours (default)
     python bench.py --impl reference                      # CPU oracle arm
 
-N > 1 (torchrun, one process per GPU): A and M are row-blocked by balanced
-work, B is broadcast from rank 0 over NCCL, the per-rank triangle sums are
-all-reduced; total work is fixed, so scaling is "strong".
+N > 1 (torchrun, one process per GPU): rank 0 builds L; B (= L) is broadcast
+over NCCL; A and M are row-blocked by balanced work, re-cut during warm-up by
+every rank's measured multiply time; the per-rank triangle sums are
+all-reduced; total work is fixed, so scaling is "strong".  The N > 1 e2e
+step is rank 0's H2D of L + the NCCL broadcast + the block multiplies + the
+all-reduce + the D2H of the count.
 """
 
 from __future__ import annotations
@@ -38,14 +41,14 @@ sys.path.insert(0, ROOT)
 METRIC = "masked-SpGEMM useful GFLOP/s & triangles/s; HBM GB/s vs roofline at 1/2/4/8 B200"
 UNIT = "useful GFLOP/s"
 EXPECTED_TRIANGLES = {20: 423909251}
-NBINS = 46          # analyze.cuh Bin::NBINS
+NBINS = 47          # analyze.cuh Bin::NBINS
 SUMMARY_BYTES = 32 + NBINS * 8 + NBINS * 4 * 4 + 16          # sizeof(mm::Summary), read back twice per multiply
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
 BIN_NAMES = (["empty"] + [f"{m}_t{t}{c}" for m in ("plain", "ctab", "csrch")
                           for t, c in ((0, "s"), (0, "l"), (1, "s"), (1, "l"), (2, "s"), (2, "l"), (3, "g"))]
              + ["pull"] + [f"{f}_t{t}" for f in ("msa", "mca", "heap") for t in range(4)] + ["single"]
              + [f"msa_sparse_t{t}" for t in range(3)] + [f"msa_dense_t{t}" for t in range(3)]
-             + [f"msa_dense_comp_t{t}" for t in range(3)] + ["pull_lane"])
+             + [f"msa_dense_comp_t{t}" for t in range(3)] + ["pull_lane", "f64_defer"])
 assert len(BIN_NAMES) == NBINS
 
 
@@ -211,8 +214,8 @@ def run_reference(args, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (seeded R-MAT, reference generator restated)",
-        "config": {"workload": f"cfg2 triangle count R-MAT s{args.scale} ef16, L.(L L) plus-pair int64",
-                   "parallelism": f"cpu threads x{workers}"},
+        "config": workload_config(args.scale),
+        "details": {"algorithm": "MSA-1P (oracle port)", "parallelism": f"cpu threads x{workers}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -222,7 +225,17 @@ def run_reference(args, rank):
     return 0
 
 
+def workload_config(scale):
+    """The workload identity — printed identically by both arms."""
+    return {"workload": f"cfg2 triangle count R-MAT s{scale} ef16, C = L.(L L) plus-pair int64",
+            "scale": scale, "edge_factor": 16, "rmat_abcd": [0.57, 0.19, 0.19, 0.05], "seed": 0,
+            "mask": "L (plain)", "semiring": "plus-pair", "values": "int64",
+            "l2": "flushed (512 MiB write) before every timed GPU step; inputs 71 MB < L2"}
+
+
 def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -230,8 +243,8 @@ def run_ours(args, rank, world, local_rank):
     from paper_2111_09947_b200 import MultiplyPlan, plus_pair_semiring
     from paper_2111_09947_b200 import _lib
     from paper_2111_09947_b200.device import DeviceCsr
-    from paper_2111_09947_b200.distributed import (allreduce_sum_, balanced_cuts, broadcast_csr,
-                                                   row_block, row_work)
+    from paper_2111_09947_b200.distributed import (RowPartition, allreduce_sum_, broadcast_csr,
+                                                   replicate_from_host, row_work_device)
     from paper_2111_09947_b200.multiply import _handle, multiply_device, reduce_sum
 
     # one process per GPU; MM_DIST_BACKEND=gloo (with fewer GPUs than ranks)
@@ -245,32 +258,36 @@ def run_ours(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    _lib.load()
-    low, t_gen = build_inputs(args.scale, on_device=True)
-    m = low.nrows
+    lib = _lib.load()
     plan = MultiplyPlan(algorithm=args.algo, semiring=plus_pair_semiring(np.int64))
 
-    # host copies (pinned) for e2e; device-resident copies for `value`
-    h_ptr = torch.from_numpy(np.ascontiguousarray(low.row_ptr, dtype=np.int64)).pin_memory()
-    h_idx = torch.from_numpy(np.ascontiguousarray(low.col_idx[: low.nnz], dtype=np.int32)).pin_memory()
-    full = DeviceCsr(m, low.ncols, h_ptr.to(dev), h_idx.to(dev), None)
+    # inputs: rank 0 generates the graph (host R-MAT stream + device
+    # canonicalisation) and keeps pinned host copies for e2e; at N > 1 the
+    # other ranks receive L by NCCL broadcast (setup, untimed)
+    t_gen = 0.0
+    low = h_ptr = h_idx = full = None
+    if rank == 0:
+        low, t_gen = build_inputs(args.scale, on_device=True)
+        h_ptr = torch.from_numpy(np.ascontiguousarray(low.row_ptr, dtype=np.int64)).pin_memory()
+        h_idx = torch.from_numpy(np.ascontiguousarray(low.col_idx[: low.nnz], dtype=np.int32)).pin_memory()
+        full = DeviceCsr(low.nrows, low.ncols, h_ptr.to(dev), h_idx.to(dev), None)
+    part = None
     if world > 1:
-        cuts = balanced_cuts(row_work(low.row_ptr, low.col_idx, low.row_ptr, low.row_ptr), world)
-        lo, hi = int(cuts[rank]), int(cuts[rank + 1])
-        b_full = broadcast_csr(full if rank == 0 else None, 0, dev)
+        b_full = broadcast_csr(full, 0, dev)
+        work = row_work_device(b_full, b_full, b_full).cpu().numpy() if rank == 0 else None
+        part = RowPartition(b_full, work, dev)
+        a_blk = part.block()
     else:
-        lo, hi = 0, m
-        b_full = full
-    a_blk = row_block(full, lo, hi) if world > 1 else full
+        b_full = a_blk = full
+    m, ncols, nnz_l = b_full.nrows, b_full.ncols, b_full.nnz
     # B^T (CSC) is only built for the pull algorithm; "auto" without it is the
-    # push-only cost model (MSA bitmap / hash tiers), so the e2e step does not
-    # pay a transpose the device-resident step would not
+    # push-only cost model (MSA bitmap / hash tiers)
     bt = b_full.transpose_storage() if args.algo == "inner" else None
     stream = torch.cuda.current_stream(dev)
-    lib = _lib.load()
-    import ctypes as C
     h = _handle(gpu)
     lib.mm_profile_enable(h, 1)
+    ms_buf = (C.c_float * 6)()
+    launches = C.c_int64(0)
 
     def step(a, b, btt):
         c, st = multiply_device(a, a, b, plan, b_csc=btt, stream=stream)
@@ -280,14 +297,27 @@ def run_ours(args, rank, world, local_rank):
         return c, st, tri
 
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    # warm-up; at N > 1 the first rounds also re-balance the cuts by every
+    # rank's measured multiply time (distributed.RowPartition.rebalance)
+    refine_rounds = min(3, max(args.warmup - 1, 0)) if world > 1 else 0
+    balance = []
     for w in range(args.warmup):
         c, st, tri = step(a_blk, b_full, bt)
+        if world > 1:
+            lib.mm_profile_read(h, ms_buf, 6, C.byref(launches))
+            if w < refine_rounds:
+                balance.append(part.rebalance(ms_buf[5]))
+                a_blk = part.block()
+            elif w == refine_rounds:
+                balance.append(part.rebalance(ms_buf[5]))   # records the last cuts' costs
+                part.use_best()
+                a_blk = part.block()
+    if world > 1 and refine_rounds >= args.warmup - 1:
+        c, st, tri = step(a_blk, b_full, bt)              # one untimed step on the final cuts
     torch.cuda.synchronize()
     tri_total = int(tri.item())
     expected = EXPECTED_TRIANGLES.get(args.scale)
 
-    ms_buf = (C.c_float * 6)()
-    launches = C.c_int64(0)
     phase = [0.0] * 6
     step_ms = []
     clocks = ClockSampler(gpu)
@@ -317,19 +347,22 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     tri_total = int(tri.item())
     my_ms = sum(step_ms) / len(step_ms)
-    evaluated_local = st.evaluated_multiplies
-    flops_local = st.generated_flops
-    nnz_c_local = c.nnz
-    if world > 1:
-        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-        tot = torch.tensor([evaluated_local, flops_local, nnz_c_local], dtype=torch.int64, device=dev)
-        dist.all_reduce(tot)
-        evaluated, flops, nnz_c = (int(x) for x in tot.tolist())
-    else:
-        ms_max, evaluated, flops, nnz_c = my_ms, evaluated_local, flops_local, nnz_c_local
     per = [p / args.steps for p in phase]
+    if world > 1:
+        t = torch.tensor([my_ms, per[2], per[5]], dtype=torch.float64, device=dev)
+        tt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tt, t)
+        rank_ms = [[float(x) for x in r.tolist()] for r in tt]
+        ms_max = max(r[0] for r in rank_ms)
+        numeric_ms_max = max(r[1] for r in rank_ms)
+        tot = torch.tensor([st.evaluated_multiplies, st.generated_flops, c.nnz, n_launch_total],
+                           dtype=torch.int64, device=dev)
+        dist.all_reduce(tot)
+        evaluated, flops, nnz_c, n_launch_total = (int(x) for x in tot.tolist())
+    else:
+        rank_ms = None
+        ms_max, numeric_ms_max = my_ms, per[2]
+        evaluated, flops, nnz_c = st.evaluated_multiplies, st.generated_flops, c.nnz
     nb = len(BIN_NAMES)
     b_rows = (C.c_int64 * nb)()
     b_flops = (C.c_int64 * nb)()
@@ -338,19 +371,30 @@ def run_ours(args, rank, world, local_rank):
             for b in range(nb) if b_rows[b]}
 
     # ---- e2e through the public API from pinned host buffers ----
+    # N = 1: H2D of L (A = B = M) -> multiply -> device sum -> D2H of the count.
+    # N > 1: rank 0's H2D of L -> NCCL broadcast of B to every rank -> each
+    # rank multiplies its row block (views, host-known offsets) -> device sum
+    # -> NCCL all-reduce -> D2H of the count.
     e2e = None
     if not args.no_e2e:
+        e_ptr = torch.empty(m + 1, dtype=torch.int64, device=dev)
+        e_idx = torch.empty(nnz_l, dtype=torch.int32, device=dev)
         e2e_ms = []
         for s in range(args.steps + 1):
             flush.fill_(s & 0xFF)
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            d_ptr = h_ptr.to(dev, non_blocking=True)
-            d_idx = h_idx.to(dev, non_blocking=True)
-            d_full = DeviceCsr(m, low.ncols, d_ptr, d_idx, None)
-            d_a = row_block(d_full, lo, hi) if world > 1 else d_full
+            if world > 1:
+                replicate_from_host([h_ptr, h_idx] if rank == 0 else None, [e_ptr, e_idx])
+            else:
+                e_ptr.copy_(h_ptr, non_blocking=True)
+                e_idx.copy_(h_idx, non_blocking=True)
+            d_full = DeviceCsr(m, ncols, e_ptr, e_idx, None)
+            d_a = part.block(d_full) if world > 1 else d_full
             d_bt = d_full.transpose_storage() if args.algo == "inner" else None
             _, _, tri_e = step(d_a, d_full, d_bt)
             tri_host = int(tri_e.item())                   # device->host read of the result
@@ -364,47 +408,30 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_t = float(t.item())
-        h2d = h_ptr.numel() * 8 + h_idx.numel() * 4
+        h2d = (m + 1) * 8 + nnz_l * 4                       # rank 0's copy of L
         e2e = {"value": evaluated / (e2e_t * 1e-3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 + 2 * SUMMARY_BYTES,
-               "ms_per_step": e2e_t}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": world * (8 + 2 * SUMMARY_BYTES),
+               "ms_per_step": e2e_t,
+               "path": ("H2D of L on rank 0 + NCCL broadcast + per-rank block multiply + all-reduce"
+                        if world > 1 else "H2D of L + multiply + device sum + D2H of the count")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         workers = oracle.use_all_cores()
         r = cpu_reference_run(low, workers)
-        t1 = time.perf_counter()
         r = cpu_reference_run(low, workers)
         cpu_t = r.total_seconds
         cpu = {"value": r.evaluated_multiplies / cpu_t / 1e9, "unit": UNIT, "cores": workers,
                "kind": "port", "seconds": cpu_t,
                "sample": "full workload, oracle MSA-1P (C restatement of the reference numba "
                          "kernels), best of 2"}
-        del t1
-
-    numeric_ms_max = per[2]
-    if world > 1:
-        # per-GPU roofline: the whole job's bytes split over N GPUs, against the
-        # slowest rank's numeric phase (every rank joins this reduction)
-        t = torch.tensor([numeric_ms_max], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        numeric_ms_max = float(t.item())
 
     if rank == 0:
         peak, peak_src = measured_peak()
-        nnz_a = low.nnz
-        bytes_alg = push_bytes(m, nnz_a, flops, nnz_a, nnz_c, 0)
-        numeric_ms = numeric_ms_max
-        achieved = bytes_alg / world / (numeric_ms * 1e-3) / 1e9
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tfile):
-            try:
-                with open(tfile) as f:
-                    traffic = json.load(f).get("numeric_bytes_per_launch")
-            except Exception:
-                traffic = None
+        bytes_alg = push_bytes(m, nnz_l, flops, nnz_l, nnz_c, 0)
+        achieved = bytes_alg / world / (numeric_ms_max * 1e-3) / 1e9
+        traffic, traffic_src = load_traffic()
         line = {
             "metric": METRIC,
             "value": evaluated / (ms_max * 1e-3) / 1e9,
@@ -418,20 +445,22 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None,
             "dtype": "int64",
             "data": "synthetic (seeded R-MAT, reference generator restated; inputs pinned by digest)",
-            "config": {"workload": f"cfg2 triangle count R-MAT s{args.scale} ef16, C = L.(L L) plus-pair int64",
-                       "algorithm": plan.label(), "nrows": m, "nnz_L": nnz_a,
-                       "generated_flops": flops, "useful_products": evaluated, "nnz_C": nnz_c,
-                       "triangles": tri_total,
-                       "triangles_ok": (tri_total == expected) if expected else None,
-                       "l2": "flushed (512 MiB write) before every timed step; inputs 71 MB < L2",
-                       "parallelism": f"row-block x{world}" if world > 1 else "1 GPU"},
+            "config": workload_config(args.scale),
+            "details": {"algorithm": plan.label(), "nrows": m, "nnz_L": nnz_l,
+                        "generated_flops": flops, "useful_products": evaluated, "nnz_C": nnz_c,
+                        "triangles": tri_total,
+                        "triangles_ok": (tri_total == expected) if expected else None,
+                        "parallelism": (f"row-block x{world} ({backend}); B broadcast from rank 0"
+                                        if world > 1 else "1 GPU")},
             "triangles_per_s": tri_total / (ms_max * 1e-3),
             "hbm_alg_gbs": bytes_alg / (ms_max * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "dram_frac": (traffic / (numeric_ms_max * 1e-3) / 1e9 / peak
+                                       if traffic and world == 1 else None),
                          "frac_of_8tbs": achieved / 8000.0,      # north_star's denominator
                          "kernel": "numeric phase: every row-bin kernel of one multiply (MSA bitmap / hash / pull tiers)",
-                         "bytes_alg_per_launch": bytes_alg, "kernel_ms": numeric_ms,
+                         "bytes_alg_per_launch": bytes_alg, "kernel_ms": numeric_ms_max,
                          "peak_source": peak_src,
                          "per_gpu": world > 1,
                          "step_frac": bytes_alg / world / (ms_max * 1e-3) / 1e9 / peak},
@@ -443,6 +472,10 @@ def run_ours(args, rank, world, local_rank):
             "wall_s_timed": t_wall,
             "input_gen_s": t_gen,
         }
+        if world > 1:
+            line["partition"] = {"cuts": part.cuts, "rank_ms": rank_ms,
+                                 "imbalance_per_refine_round": balance,
+                                 "refine": "warm-up rounds re-cut by measured per-rank multiply ms"}
         if e2e:
             line["e2e"] = e2e
         if cpu:
@@ -451,6 +484,24 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def load_traffic():
+    """DRAM bytes (read + write) per multiply of the numeric kernels, from the
+    committed ncu capture (profiles/ncu_traffic.json), with its provenance."""
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tfile):
+        return None, None
+    try:
+        with open(tfile) as f:
+            d = json.load(f)
+    except Exception:
+        return None, None
+    src = {"file": "profiles/ncu_traffic.json"}
+    for k in ("source", "commit", "config", "command", "captured"):
+        if k in d:
+            src[k] = d[k]
+    return d.get("numeric_bytes_per_launch"), src
 
 
 def main():

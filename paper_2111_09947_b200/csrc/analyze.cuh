@@ -34,7 +34,8 @@ enum Bin : int {
     BIN_MSAD0 = 39,   // + tier (0..2): MSA with a dense per-column window (push_dense.cuh)
     BIN_MSADC0 = 42,  // + tier (0..2): complemented MSA over every column (narrow outputs)
     BIN_PULL_LANE = 45,  // pull, one lane per mask entry (short masks, short A rows and B columns)
-    NBINS = 46
+    BIN_F64D = 46,       // ordered float64, plain hash with deferred hits (push_f64_defer.cuh)
+    NBINS = 47
 };
 __host__ __device__ constexpr bool is_msadc_bin(int b) { return b >= BIN_MSADC0 && b < BIN_MSADC0 + 3; }
 __host__ __device__ constexpr bool is_msas_bin(int b) { return b >= BIN_MSAS0 && b < BIN_MSAS0 + 3; }
@@ -118,6 +119,16 @@ __host__ __device__ constexpr int64_t mca_bytes(int64_t nm, int kind) {
     return (kind == 0 ? 8 : 16) * nm;
 }
 
+// Largest mask row of the deferred-hit float64 bin (its table: 2^8..2^9 slots).
+constexpr int64_t F64D_MAX_NM = 256;
+
+// The symbolic pass of that bin runs the plain tier-0 hash kernel: its table size.
+__device__ __forceinline__ int f64d_bin(int64_t nm, int* cap_lg_out) {
+    const int lg = ceil_log2_i64(4 * nm);
+    *cap_lg_out = lg < 5 ? 5 : lg;
+    return BIN_F64D;
+}
+
 // Chooses the bin for a row and the table size (log2) the row will use.
 // words = 32-column words spanned by the mask row (MSA window).
 __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na, int64_t nm,
@@ -143,6 +154,9 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             int64_t push = 16 * na + flops * w;
             int64_t pull = 16 * nm + (nm * na + pull_cols) * w;
             if (ap.has_bt && pull < push) fam = FAM_PULL;
+            // ordered float64 single-warp rows with short masks: the direct /
+            // cuckoo hash probe with hits folded in k order afterwards
+            else if (ap.ordered && tf == 0 && nm <= F64D_MAX_NM) return f64d_bin(nm, cap_lg_out);
             // ordered float64 rows (one warp, k order): the rank search beats
             // both the bitmap and the hash for short mask rows
             else if (ap.ordered && nm <= 512 && msad_bytes(words, kind) > ap.rank_budget[tf]) fam = FAM_MCA;
@@ -158,13 +172,20 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     }
     if (fam == FAM_HEAP) {
         // plain: mask-rank slots in shared memory (tier 0) or global (tier 1);
-        // complement rows with <= 32 A entries: sorted single-batch merge (2)
+        // complement rows with <= 32 A entries: sorted single-batch merge (2),
+        // more A entries: the multi-iterator merge (3)
         if (!ap.comp) {
             const int64_t bytes = (kind == 0 ? 4 : 12) * nm;
             return BIN_HEAP0 + (bytes <= ap.rank_budget[0] ? 0 : 1);
         }
         if (na <= 32) return BIN_HEAP0 + 2;
+        // wider complement rows: every A entry an iterator (k_push_heap_comp);
+        // the bin keeps its largest A row in bin_words
+        *aux_out = na;
+        return BIN_HEAP0 + 3;
     }
+    // the hash plan's ordered single-warp plain rows: same deferred form
+    if (fam == FAM_HASH && ap.ordered && !ap.comp && tf == 0 && nm <= F64D_MAX_NM) return f64d_bin(nm, cap_lg_out);
     const bool single_ok = !ap.ordered || tf == 0;
     if (!ap.comp && fam == FAM_MSA && single_ok && msa_bytes(words, nm, kind) > ap.rank_budget[tr] &&
         msas_bytes(words, nm, kind) <= ap.rank_budget[tr] && nm < 65536) {

@@ -27,6 +27,7 @@
 #include "push_single.cuh"
 #include "push_msa_sparse.cuh"
 #include "push_dense.cuh"
+#include "push_f64_defer.cuh"
 #include "scan_compact.cuh"
 #include "graph_ops.cuh"
 #include "graph_prep.cuh"
@@ -580,6 +581,59 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             CU(cudaGetLastError());
             continue;
         }
+        if (b == BIN_F64D) {
+            // ordered float64, deferred hits: symbolic runs the plain
+            // order-free hash kernel (counts only)
+            if (!numeric || h->kind != 2) {
+                int gw = 1;
+                HashKernel kern = pick_hash(0, MODE_PLAIN, 0, false, &gw);
+                if (numeric) return fail(MM_ERR_INTERNAL, "deferred float64 bin without float64 values");
+                const int cap_lg = std::max(h->sum.bin_cap_lg[b], 5);
+                const size_t smem = 8 * (((size_t)8 << cap_lg) + batch_bytes_rt(1, 0)) + 8 * (size_t)64 * 8;
+                int occ = 0;
+                if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
+                const int grid = std::max(1, std::min((cnt + 7) / 8, std::max(occ, 1) * h->num_sms));
+                ++g_launches;
+                kern<<<grid, 256, smem, st>>>(h->prob, out, wk, h->row_cap_lg, cap_lg, nullptr);
+                CU(cudaGetLastError());
+                continue;
+            }
+            const int nm_max = std::max(h->sum.bin_nmmax[b], 1);
+            const size_t smem = 8 * defer_warp_bytes(nm_max);
+            int occ = 0;
+            if ((rc = kernel_occupancy((const void*)k_push_f64_defer<true>, 256, smem, &occ))) return rc;
+            const int grid = std::max(1, std::min((cnt + 7) / 8, std::max(occ, 1) * h->num_sms));
+            ++g_launches;
+            if (debug_launches())
+                fprintf(stderr, "[mm] f64-defer bin rows %d nm_max %d smem %zu grid %d occ %d\n", cnt, nm_max, smem,
+                        grid, occ);
+            k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max);
+            CU(cudaGetLastError());
+            continue;
+        }
+        if (b == BIN_HEAP0 + 3) {
+            // complemented heap rows with > 32 A entries: iterator state in a
+            // per-warp global slab sized by the bin's widest A row
+            const int kind = numeric ? h->kind : 0;
+            void (*kern)(Prob, Out, Work, int, unsigned char*) = nullptr;
+            if (!numeric) kern = k_push_heap_comp<0, false>;
+            else if (kind == 0) kern = k_push_heap_comp<0, true>;
+            else if (kind == 1) kern = k_push_heap_comp<1, true>;
+            else kern = k_push_heap_comp<2, true>;
+            const int na_max = std::max(h->sum.bin_words[b], 1);
+            const size_t per_block = 8 * heap_iter_bytes(na_max);
+            int occ = 0;
+            if ((rc = kernel_occupancy((const void*)kern, 256, 0, &occ))) return rc;
+            int grid = std::max(1, std::min((cnt + 7) / 8, std::max(occ, 1) * h->num_sms));
+            grid = (int)std::max<size_t>(1, std::min<size_t>(grid, ((size_t)1 << 30) / per_block));
+            unsigned char* gslab = nullptr;
+            CU(cudaMallocAsync((void**)&gslab, (size_t)grid * per_block, st));
+            h->allocs.push_back(gslab);
+            ++g_launches;
+            kern<<<grid, 256, 0, st>>>(h->prob, out, wk, na_max, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
         if (is_heap_bin(b)) {
             const int sub = b - BIN_HEAP0;
             const bool comp_rows = sub == 2;
@@ -975,7 +1029,20 @@ int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_value
         CU(cudaMemcpyAsync(c_row_ptr, h->c_row_ptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     int* flag = &h->d_summary->flag;
     if (h->plan.phases == 1) {
-        if (m > 0) {
+        if (m > 0 && h->total_nnz <= 2 * m) {
+            // sparse outputs: a thread per row
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
+            ++g_launches;
+            if (h->out_f64)
+                k_compact_rowwise<double><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
+                                                                (const double*)h->tmp_val, h->c_row_ptr,
+                                                                c_col_idx, (double*)c_values, nullptr);
+            else
+                k_compact_rowwise<long long><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
+                                                                   (const long long*)h->tmp_val, h->c_row_ptr,
+                                                                   c_col_idx, (long long*)c_values, nullptr);
+            CU(cudaGetLastError());
+        } else if (m > 0) {
             int64_t want = std::max<int64_t>((h->total_nnz + 2047) / 2048, (m + 255) / 256);
             int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)h->num_sms * 16));
             ++g_launches;

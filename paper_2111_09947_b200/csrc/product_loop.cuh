@@ -121,10 +121,12 @@ struct RowFetcher {
 };
 
 // Shared-memory staging of one batch of A entries: base of the B row (made
-// relative to the batch's product index), A value (int64 plus-times), and
-// the inclusive product end.  Bytes per group.
+// relative to the batch's product index), the carried A word (int64 plus-times:
+// the A value; KIND 3, ordered float64 with deferred hits: the A position),
+// and the inclusive product end.  Bytes per group.
+__host__ __device__ constexpr bool carries_a(int kind) { return kind == 1 || kind == 3; }
 __host__ __device__ constexpr size_t batch_bytes_rt(int gw, int kind) {
-    return kind == 2 ? 0 : (size_t)gw * 32 * ((kind == 1 ? 16 : 8) + 4);
+    return kind == 2 ? 0 : (size_t)gw * 32 * ((carries_a(kind) ? 16 : 8) + 4);
 }
 template <int GW, int KIND>
 __host__ __device__ constexpr size_t batch_bytes() {
@@ -143,7 +145,7 @@ __device__ __forceinline__ BatchSmem bind_batch(unsigned char* bbase) {
     BatchSmem bsm;
     bsm.base = (long long*)bbase;
     bsm.av = bsm.base + GT;
-    bsm.incl = (int32_t*)(bbase + (size_t)GT * (KIND == 1 ? 16 : 8));
+    bsm.incl = (int32_t*)(bbase + (size_t)GT * (carries_a(KIND) ? 16 : 8));
     return bsm;
 }
 
@@ -180,6 +182,7 @@ __device__ __forceinline__ void tail_chunk(const Prob& p, PR& pr, const int32_t*
 //   [c_lo, c_hi): only products with a column in this range (a sub-range of
 //   each sorted B row, by binary search); the default is every product.
 //
+//   KIND 3 carries the A position t in the `a` word instead of a value.
 //   SEARCH (plain masks): an A entry whose B row is much longer than the
 //   mask part [srch_m, srch_m + srch_nm) makes nm·log2(len) probes instead
 //   of len — each mask column is binary-searched in B_k, and only the columns
@@ -207,6 +210,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
     constexpr int U = MM_PRODUCT_UNROLL;   // independent B loads in flight per lane
     constexpr int CH = 32 * U;
     constexpr int NB = GT;
+    constexpr bool CARRY = carries_a(KIND);
     const int lane32 = gt & 31;
     for (int64_t tb0 = as; tb0 < ae; tb0 += NB) {
         const int64_t t = tb0 + gt;
@@ -220,6 +224,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
             if (c_hi != INT32_MAX) end = lower_bound_range(p.b_idx, base, end, c_hi);
             len = (int)(end - base);
             if (KIND == 1) av = ((const long long*)p.a_val)[t];
+            if (KIND == 3) av = t;
         }
         bool srch = false;
         if (SEARCH && len > 0) {
@@ -234,7 +239,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
         if (GW > 1) {
             bsm.incl[gt] = incl;
             bsm.base[gt] = base - (incl - flen);
-            if (KIND == 1) bsm.av[gt] = av;
+            if (CARRY) bsm.av[gt] = av;
             group_bar(bar_id, GT);
             const int wg = gt >> 5;
             q_lo = (int)(((long long)tot * wg) / GW);
@@ -267,7 +272,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 const int a1 = e_in < q_hi ? e_in : q_hi;
                 plen = a1 > a0 ? a1 - a0 : 0;
                 sb = bsm.base[l] + a0;
-                if (KIND == 1) sa = bsm.av[l];
+                if (CARRY) sa = bsm.av[l];
             }
             unsigned longm = __ballot_sync(FULL, plen >= 32);
             while (longm) {
@@ -275,7 +280,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 longm &= longm - 1;
                 const long long b0 = shfl64(sb, src);
                 const int n0 = __shfl_sync(FULL, plen, src);
-                const long long a0 = KIND == 1 ? __shfl_sync(FULL, sa, src) : 0;
+                const long long a0 = CARRY ? shfl64(sa, src) : 0;
                 const int32_t* bp = p.b_idx + b0;
                 int c = 0;
                 for (; c + CH <= n0; c += CH) {   // full chunks: no bounds predicates
@@ -312,7 +317,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                         const int q = w0 + 32 * u + lane32;
                         const int own = owner_of(sincl, q < stot ? q : stot - 1);
                         ss[u] = shfl64(sb, own) + (q - __shfl_sync(FULL, sexcl, own));
-                        aa[u] = KIND == 1 ? __shfl_sync(FULL, sa, own) : 0;
+                        aa[u] = CARRY ? shfl64(sa, own) : 0;
                         jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
                     }
                     pr.template put_batch<2>(jj, aa, ss);
@@ -332,7 +337,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 const long long c_rel = shfl64(sb - sexcl, src);
                 const int ex = __shfl_sync(FULL, sexcl, src);
                 const int c_ex = lane32 < ns ? ex : 0x7fffffff;
-                const long long c_a = KIND == 1 ? shfl64(sa, src) : 0;
+                const long long c_a = CARRY ? shfl64(sa, src) : 0;
                 const unsigned upto = 0xffffffffu >> (31 - lane32);
                 for (int w0 = 0; w0 < stot; w0 += 64) {
                     int32_t jj[2];
@@ -346,7 +351,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                         const int own = c0 + __popc(starts & upto);
                         const int q = wb + lane32;
                         ss[u] = shfl64(c_rel, own) + q;
-                        aa[u] = KIND == 1 ? shfl64(c_a, own) : 0;
+                        aa[u] = CARRY ? shfl64(c_a, own) : 0;
                         jj[u] = q < stot ? __ldg(p.b_idx + ss[u]) : EMPTY_KEY;
                     }
                     pr.template put_batch<2>(jj, aa, ss);
@@ -364,7 +369,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 if (srch) {
                     bsm.base[sincl - 1] = base;
                     bsm.incl[sincl - 1] = len;
-                    if (KIND == 1) bsm.av[sincl - 1] = av;
+                    if (CARRY) bsm.av[sincl - 1] = av;
                 }
                 if (GW > 1) group_bar(bar_id, GT); else __syncwarp();
                 // SU interleaved branch-free lower bounds per lane: their
@@ -390,7 +395,7 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                             ss[u] = bsm.base[item];
                             bb[u] = p.b_idx + ss[u];
                             nn[u] = bsm.incl[item];
-                            if (KIND == 1) aa[u] = bsm.av[item];
+                            if (CARRY) aa[u] = bsm.av[item];
                         }
                     }
                     const int32_t* b0[SU];

@@ -208,3 +208,144 @@ __global__ void __launch_bounds__(256) k_push_heap(Prob p, Out o, Work wk, int n
 }
 
 }  // namespace mm
+
+namespace mm {
+
+// Complemented heap rows with more than 32 A entries: every A entry of the
+// row is an iterator (the reference pushes them all into one heap,
+// _kernels.py:444-447, NInspect forced to 0 for the complement, :437).
+// Lane l owns iterators q = l + 32u (u < K = ceil(na / 32)), their state in
+// the warp's slab: head column, remaining length, B position.  The lane keeps
+// the minimum head of its iterators; the warp-wide minimum is the heap's pop
+// (__reduce_min_sync), the mask cursor advances to it, and every iterator
+// sitting on that column contributes and advances.  Contributions fold in
+// ascending A position (u-major, then lane: ascending k, the MSA order, so a
+// float64 slot is bit-identical to MSA); the output arrives column-sorted.
+// Per-iterator bytes in the slab: 4 (head) + 4 (remaining) + 8 (position).
+__host__ __device__ constexpr size_t heap_iter_bytes(int64_t na_max) {
+    return (size_t)16 * (size_t)((na_max + 31) & ~31ll);
+}
+
+template <int KIND, bool NUMERIC>
+__global__ void __launch_bounds__(256) k_push_heap_comp(Prob p, Out o, Work wk, int na_max, unsigned char* gslab) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t cap = (na_max + 31) & ~31;
+    unsigned char* slab = gslab + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * heap_iter_bytes(na_max);
+    uint32_t* s_head = (uint32_t*)slab;
+    uint32_t* s_rem = s_head + cap;
+    int64_t* s_pos = (int64_t*)(s_rem + cap);
+    unsigned long long evaluated = 0;
+    for (;;) {
+        int r = 0;
+        if (lane == 0) r = atomicAdd(wk.cursor, 1);
+        r = __shfl_sync(FULL, r, 0);
+        if (r >= wk.count) break;
+        const int64_t i = wk.rows[r];
+        const int64_t as = p.a_ptr[i], ae = p.a_ptr[i + 1];
+        const int64_t ms = p.m_ptr[i], nm = p.m_ptr[i + 1] - ms;
+        const int32_t* m = p.m_idx + ms;
+        const int64_t w0 = NUMERIC ? o.off[i] : 0;
+        const int na = (int)(ae - as);
+        const int K = (na + 31) >> 5;
+        // load every iterator; lane minimum
+        uint32_t lmin = HEAP_DONE;
+        for (int u = 0; u < K; u++) {
+            const int q = u * 32 + lane;
+            uint32_t head = HEAP_DONE;
+            if (q < na) {
+                const int32_t k = p.a_idx[as + q];
+                const int64_t b0 = p.b_ptr[k], b1 = p.b_ptr[k + 1];
+                s_pos[q] = b0;
+                s_rem[q] = (uint32_t)(b1 - b0);
+                head = b1 > b0 ? (uint32_t)p.b_idx[b0] : HEAP_DONE;
+                s_head[q] = head;
+            }
+            lmin = min(lmin, head);
+        }
+        __syncwarp();
+        int64_t mcur = 0, n_out = 0;
+        for (;;) {
+            const uint32_t c = __reduce_min_sync(FULL, lmin);
+            if (c == HEAP_DONE) break;
+            mcur = mask_advance(m, mcur, nm, (int32_t)c, lane);
+            const bool hit = !(mcur < nm && m[mcur] == (int32_t)c);
+            const bool mine = lmin == c;
+            long long isum = 0;
+            double acc = 0.0;
+            bool first = true;
+            int contrib = 0;
+            uint32_t nmin = HEAP_DONE;
+            if (KIND == 2) {
+                // ascending A position: u-major, lanes in order inside u
+                for (int u = 0; u < K; u++) {
+                    const int q = u * 32 + lane;
+                    const bool on = mine && q < na && s_head[q] == c;
+                    unsigned b = __ballot_sync(FULL, on);
+                    double prod = 0.0;
+                    if (on && hit && NUMERIC) prod = ((const double*)p.a_val)[as + q] * ((const double*)p.b_val)[s_pos[q]];
+                    while (b) {
+                        const int src = __ffs(b) - 1;
+                        b &= b - 1;
+                        const double pb = __shfl_sync(FULL, prod, src);
+                        acc = first ? pb : acc + pb;
+                        first = false;
+                        contrib++;
+                    }
+                }
+            }
+            if (mine) {
+                // advance every iterator of this lane on column c
+                for (int u = 0; u < K; u++) {
+                    const int q = u * 32 + lane;
+                    if (q >= na) break;
+                    uint32_t head = s_head[q];
+                    if (head == c) {
+                        const int64_t pos = s_pos[q];
+                        if (KIND != 2) {
+                            contrib++;
+                            if (NUMERIC && hit)
+                                isum += KIND == 1 ? ((const long long*)p.a_val)[as + q] * ((const long long*)p.b_val)[pos] : 1;
+                        }
+                        const uint32_t rem = s_rem[q] - 1;
+                        s_rem[q] = rem;
+                        s_pos[q] = pos + 1;
+                        head = rem ? (uint32_t)p.b_idx[pos + 1] : HEAP_DONE;
+                        s_head[q] = head;
+                    }
+                    nmin = min(nmin, head);
+                }
+                lmin = nmin;
+            }
+            __syncwarp();
+            if (hit) {
+                if (KIND == 2) {
+                    if (lane == 0) {
+                        evaluated += contrib;
+                        if (NUMERIC) {
+                            o.idx[w0 + n_out] = (int32_t)c;
+                            ((double*)o.val)[w0 + n_out] = acc;
+                        }
+                    }
+                } else {
+                    const long long cnt = warp_sum_ll(contrib);
+                    const long long sum = warp_sum_ll(isum);
+                    if (lane == 0) {
+                        evaluated += cnt;
+                        if (NUMERIC) {
+                            o.idx[w0 + n_out] = (int32_t)c;
+                            if (KIND == 0 && o.out_f64) ((double*)o.val)[w0 + n_out] = (double)sum;
+                            else ((long long*)o.val)[w0 + n_out] = sum;
+                        }
+                    }
+                }
+                n_out++;
+            }
+        }
+        if (lane == 0) o.row_nnz[i] = n_out;
+        __syncwarp();
+    }
+    if (NUMERIC && lane == 0 && evaluated) atomicAdd(o.evaluated, evaluated);
+}
+
+}  // namespace mm

@@ -186,3 +186,88 @@ def gather_to_rank0(part: DeviceCsr, device) -> DeviceCsr | None:
             dist.recv(vals, r)
         parts.append(DeviceCsr(nr, part.ncols, ptr, idx, vals))
     return concat_row_blocks(parts)
+
+
+def _bcast_host_list(vals: list[int] | None, n: int, src: int, device) -> list[int]:
+    t = torch.zeros(n, dtype=torch.int64, device=device)
+    if dist.get_rank() == src:
+        t.copy_(torch.as_tensor(vals, dtype=torch.int64))
+    dist.broadcast(t, src)
+    return [int(x) for x in t.tolist()]
+
+
+class RowPartition:
+    """One rank's share of the row-partitioned multiply (bench.py --gpus N,
+    tests/test_distributed_gloo.py).
+
+    B (= the whole operand) is replicated from rank 0; this rank's A and M are
+    the row block [cuts[rank], cuts[rank+1]) of their full matrices, taken as
+    views with host-known offsets (no host sync per step).  Cuts start
+    flop-balanced (``balanced_cuts`` of rank 0's work estimate) and can be
+    re-balanced from the per-rank measured cost (``rebalance``)."""
+
+    def __init__(self, b: DeviceCsr, work: np.ndarray | None, device):
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.b = b
+        self.device = device
+        self.work = work                     # rank 0 only: per-row work estimate
+        cuts = balanced_cuts(work, self.world) if self.rank == 0 else None
+        self._set_cuts(cuts)
+        self.history = []                    # (cuts, per-rank cost) of every rebalance round
+
+    def _set_cuts(self, cuts):
+        self.cuts = _bcast_host_list(None if cuts is None else [int(x) for x in cuts], self.world + 1, 0,
+                                     self.device)
+        self.offsets = cut_offsets(self.b, self.cuts)
+
+    @property
+    def lo(self) -> int:
+        return self.cuts[self.rank]
+
+    @property
+    def hi(self) -> int:
+        return self.cuts[self.rank + 1]
+
+    def block(self, m: DeviceCsr | None = None) -> DeviceCsr:
+        """This rank's row block of m (default: of B, when A = M = B as in
+        cfg2 / cfg5).  m must have B's row pointer for the cached offsets."""
+        m = self.b if m is None else m
+        r = self.rank
+        return row_block(m, self.lo, self.hi, self.offsets[r], self.offsets[r + 1])
+
+    def costs(self, my_cost: float) -> list[float]:
+        t = torch.zeros(self.world, dtype=torch.float64, device=self.device)
+        t[self.rank] = float(my_cost)
+        dist.all_reduce(t)
+        return [float(x) for x in t.tolist()]
+
+    def rebalance(self, my_cost: float) -> float:
+        """Gather every rank's measured cost of its block, re-cut on rank 0
+        (``refine_cuts``), broadcast.  Returns the max/mean imbalance of the
+        costs just measured."""
+        c = self.costs(my_cost)
+        self.history.append((list(self.cuts), c))
+        cuts = refine_cuts(self.work, self.cuts, c, self.world) if self.rank == 0 else None
+        self._set_cuts(cuts)
+        return imbalance(c)
+
+    def use_best(self) -> float:
+        """Return to the measured cuts with the smallest maximum cost."""
+        if not self.history:
+            return 1.0
+        cuts, c = min(self.history, key=lambda h: max(h[1]))
+        self._set_cuts(cuts if self.rank == 0 else None)
+        return imbalance(c)
+
+
+def replicate_from_host(host: list[torch.Tensor] | None, dev: list[torch.Tensor], src: int = 0):
+    """The multi-GPU input path: rank `src` copies its pinned host buffers into
+    its device buffers, then every buffer is broadcast to the other ranks
+    (NCCL over NVLink on GPUs).  dev: preallocated, same shapes on every rank."""
+    if dist.get_rank() == src:
+        for h, d in zip(host, dev):
+            d.copy_(h, non_blocking=True)
+    for d in dev:
+        if d.numel():
+            dist.broadcast(d, src)

@@ -69,6 +69,67 @@ def _worker(rank, world, port, out_q):
         dist.destroy_process_group()
 
 
+def _worker_partition(rank, world, port, out_q):
+    """bench.py's N > 1 driver objects on CPU: RowPartition (flop-balanced
+    cuts on rank 0, broadcast, host-known block offsets, cost re-balancing)
+    and replicate_from_host (rank 0's host buffers -> every rank)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2111_09947_b200 import workloads
+        from paper_2111_09947_b200.device import DeviceCsr
+        from paper_2111_09947_b200.distributed import (RowPartition, allreduce_sum_, replicate_from_host,
+                                                       row_work)
+        from paper_2111_09947_b200.sparse import CsrMatrix
+
+        dev = torch.device("cpu")
+        low = workloads.triangle_lower(12)
+        m, nnz = low.nrows, low.nnz
+        h = [torch.from_numpy(low.row_ptr.copy()), torch.from_numpy(low.col_idx[:nnz].astype(np.int32))]
+        d = [torch.zeros(m + 1, dtype=torch.int64), torch.zeros(nnz, dtype=torch.int32)]
+        replicate_from_host(h if rank == 0 else None, d)
+        b = DeviceCsr(m, low.ncols, d[0], d[1], None)
+        work = row_work(low.row_ptr, low.col_idx, low.row_ptr, low.row_ptr) if rank == 0 else None
+        part = RowPartition(b, work, dev)
+        b_h = CsrMatrix(m, low.ncols, low.row_ptr, low.col_idx, np.ones(nnz, dtype=np.int64))
+        whole = oracle.masked_multiply(low.pattern(), low, low, semiring_id=1)
+        seen = []
+        for rnd in range(3):
+            blk = part.block()
+            assert (blk.nrows, int(blk.ptr[-1])) == (part.hi - part.lo, part.offsets[rank + 1] - part.offsets[rank])
+            a_h = CsrMatrix(blk.nrows, blk.ncols, blk.ptr.numpy().astype(np.int64),
+                            blk.idx.numpy().astype(np.int64), np.ones(blk.nnz, dtype=np.int64))
+            r = oracle.masked_multiply(a_h.pattern(), a_h, b_h, semiring_id=1)
+            tri = allreduce_sum_(torch.tensor([int(r.values.sum())], dtype=torch.int64))
+            assert int(tri.item()) == int(whole.values.sum())
+            # an artificial per-rank cost: rank 0's rows cost 3x their work
+            cost = float(r.generated_flops) * (3.0 if rank == 0 else 1.0)
+            seen.append((list(part.cuts), part.rebalance(cost)))
+        part.use_best()
+        if rank == 0:
+            out_q.put(seen)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_partition_driver_rebalances():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_partition, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+        assert pr.exitcode == 0
+    seen = q.get(timeout=10)
+    # the re-cut moves rows away from the expensive rank and lowers the imbalance
+    assert seen[1][0][1] < seen[0][0][1]
+    assert seen[1][1] < seen[0][1]
+
+
 @pytest.mark.parametrize("world", [2])
 def test_row_partition_broadcast_allreduce_concat(world):
     ctx = mp.get_context("spawn")
