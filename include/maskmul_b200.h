@@ -47,7 +47,7 @@ enum {
     MM_ALGO_AUTO = 6
 };
 
-enum { MM_OK = 0, MM_ERR_PLAN = 1, MM_ERR_INPUT = 2, MM_ERR_INTERNAL = 3, MM_ERR_CUDA = 4 };
+enum { MM_OK = 0, MM_ERR_PLAN = 1, MM_ERR_INPUT = 2, MM_ERR_INTERNAL = 3, MM_ERR_CUDA = 4, MM_ERR_CAPACITY = 5 };
 
 /* semiring.py:23-24 kernel_id */
 enum { MM_SR_ARITHMETIC = 0, MM_SR_PLUS_PAIR = 1 };
@@ -124,6 +124,17 @@ int mm_multiply_begin(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* 
 int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_values,
                     mm_stats_t* stats);
 
+/* One-call form of the two calls above for callers that can bound nnz(C) in
+ * advance (a plain mask: nnz(C) <= nnz(M), the one-phase bound of
+ * multiply.py:233): c_col_idx / c_values hold `capacity` entries, c_row_ptr
+ * nrows + 1 (written by the row-pointer scan itself); one host sync (the
+ * nnz readback), compaction queued right after it.  If nnz(C) > capacity it
+ * returns MM_ERR_CAPACITY with *out_nnz set and the handle still holding
+ * the multiply: allocate nnz(C) entries and finish with mm_multiply_end. */
+int mm_multiply(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+                const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* c_row_ptr,
+                int32_t* c_col_idx, void* c_values, int64_t capacity, int64_t* out_nnz, mm_stats_t* stats);
+
 /* Per-phase device timing (CUDA events recorded on the caller's stream) of
  * every later multiply on this handle; off by default.  mm_profile_read
  * waits for the last multiply and returns ms[0..5] = {analyze + bin summary,
@@ -143,7 +154,10 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
  * params[8..10] = log2 of the smallest plain shared-memory hash table in the
  * 1-, 4- and 16-warp tiers, which leaves room for a collision-free
  * (direct-mapped) table (9, 10, 12; 0 = bin size; negative keeps),
- * params[11] = params[3] for plain rows of the 16-warp tier (1). */
+ * params[11] = params[3] for plain rows of the 16-warp tier (1),
+ * params[12] / params[13] = row / nnz limits of the single-pass small-problem
+ * path (32768 / 2^20; 0 disables it), params[14] = 0 disables the direct
+ * path of ordered float64 plain one-phase multiplies (no analysis pass). */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

@@ -12,11 +12,11 @@ import os
 from .build import LIB_PATH, MMIO_LIB_PATH
 
 MM_ALGO = {"msa": 0, "hash": 1, "mca": 2, "heap": 3, "heapdot": 4, "inner": 5, "auto": 6}
-MM_OK, MM_ERR_PLAN, MM_ERR_INPUT, MM_ERR_INTERNAL, MM_ERR_CUDA = 0, 1, 2, 3, 4
+MM_OK, MM_ERR_PLAN, MM_ERR_INPUT, MM_ERR_INTERNAL, MM_ERR_CUDA, MM_ERR_CAPACITY = 0, 1, 2, 3, 4, 5
 MM_DTYPE_INT64, MM_DTYPE_FLOAT64 = 0, 1
 
 # every symbol declared in include/maskmul_b200.h
-EXPORTS = ("mm_abi_version", "mm_last_error", "mm_create", "mm_destroy", "mm_multiply_begin",
+EXPORTS = ("mm_abi_version", "mm_last_error", "mm_create", "mm_destroy", "mm_multiply", "mm_multiply_begin",
            "mm_multiply_end", "mm_symbolic", "mm_row_flops", "mm_exclusive_scan",
            "mm_compact_rows", "mm_reduce_sum", "mm_profile_enable", "mm_profile_read",
            "mm_profile_bins", "mm_set_tuning", "mm_filter_min", "mm_lookup_rows",
@@ -62,6 +62,8 @@ def load(path: str | None = None):
     lib.mm_destroy.argtypes = [P]
     lib.mm_multiply_begin.argtypes = [P, C.POINTER(PlanT), PM, PM, PM, PM, P, C.POINTER(C.c_int64)]
     lib.mm_multiply_end.argtypes = [P, P, P, P, C.POINTER(StatsT)]
+    lib.mm_multiply.argtypes = [P, C.POINTER(PlanT), PM, PM, PM, PM, P, P, P, P, C.c_int64, C.POINTER(C.c_int64),
+                                C.POINTER(StatsT)]
     lib.mm_symbolic.argtypes = [P, C.POINTER(PlanT), PM, PM, PM, PM, P, P]
     lib.mm_row_flops.argtypes = [PM, PM, P, P, P]
     lib.mm_exclusive_scan.argtypes = [P, C.c_int64, P, P]

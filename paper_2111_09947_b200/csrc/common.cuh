@@ -37,6 +37,8 @@ struct Out {
     unsigned long long* evaluated;
     int out_f64;  // 1: values are float64, 0: int64
     int* overflow;  // small-problem path: set when a row does not fit the fixed table (host falls back)
+    unsigned long long* gen_flops;   // direct path (no analysis pass): generated flops summed by the kernel
+    int* empty_rows;                 // direct path: rows with no product or an empty mask row
 };
 
 // A bin of rows handled by one kernel family/tier, fetched dynamically.

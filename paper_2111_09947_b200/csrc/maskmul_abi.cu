@@ -192,6 +192,8 @@ struct mm_handle {
     int auto_mca_nm = 0;
     int direct_lg[3] = {9, 10, 12};    // plain shared hash tables per tier: at least 2^direct_lg slots (0 = bin size)
     int64_t tiny_rows = 1 << 15, tiny_nnz = 1 << 20;   // single-pass path for small plain 1P multiplies
+    bool direct_on = true;                              // direct path for ordered float64 (see begin_impl)
+    int64_t* user_row_ptr = nullptr;                    // mm_multiply: C's row pointer, written by the scan
     // ---- concurrent bin launches ----
     static constexpr int NAUX = 3;
     cudaStream_t aux[NAUX] = {};
@@ -607,7 +609,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             if (debug_launches())
                 fprintf(stderr, "[mm] f64-defer bin rows %d nm_max %d smem %zu grid %d occ %d\n", cnt, nm_max, smem,
                         grid, occ);
-            k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max);
+            k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max, 0ll);
             CU(cudaGetLastError());
             continue;
         }
@@ -848,7 +850,8 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     int32_t* long_rows = (int32_t*)(slab + o_long);
     h->row_flops = (int64_t*)(slab + o_flops);
     h->row_nnz = (int64_t*)(slab + o_nnz);
-    h->c_row_ptr = (int64_t*)(slab + o_ptr);
+    // mm_multiply hands in the caller's row pointer: the scan writes it directly
+    h->c_row_ptr = h->user_row_ptr ? h->user_row_ptr : (int64_t*)(slab + o_ptr);
     h->bound = need_bound ? (int64_t*)(slab + o_bound) : nullptr;
     h->bound_ptr = need_bound ? (int64_t*)(slab + o_bptr) : nullptr;
     h->scan_scratch = (int64_t*)(slab + o_scan);
@@ -861,7 +864,8 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     trace("slab");
     CU(cudaMemsetAsync(h->d_summary, 0, zero_bytes, st));
 
-    if (m > 0) {
+    auto run_analysis = [&]() -> int {
+        if (m <= 0) return MM_OK;
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
         int64_t* zero_nnz = symbolic_only ? nullptr : h->row_nnz;
         ++g_launches;
@@ -875,16 +879,73 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
                                                             long_n);
             CU(cudaGetLastError());
         }
+        return MM_OK;
+    };
+    // ---- direct path for ordered float64 plain one-phase multiplies: no
+    // analysis pass — the deferred-hit kernel takes every row, sums the
+    // generated flops itself, and flags rows it cannot take (mask row over
+    // F64D_MAX_NM, products over the 4-warp tier bound); one host sync.  A
+    // flagged multiply continues on the binned path below.
+    const bool direct = plain_1p && h->kind == 2 && m > 0 && !use_bt && h->direct_on &&
+                        (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH);
+    bool have_summary = false;
+    if (direct) {
+        h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
+        Out o{};
+        o.off = h->bound_off;
+        o.idx = h->tmp_idx;
+        o.val = h->tmp_val;
+        o.row_nnz = h->row_nnz;
+        o.evaluated = &h->d_summary->evaluated;
+        o.out_f64 = 1;
+        o.overflow = &h->d_summary->pad;
+        o.gen_flops = &h->d_summary->gen_flops;
+        o.empty_rows = &h->d_summary->bin_count[BIN_EMPTY];
+        const int nm_max = (int)F64D_MAX_NM;
+        const size_t smem = 8 * defer_warp_bytes(nm_max);
+        int occ = 0;
+        if ((rc = kernel_occupancy((const void*)k_push_f64_defer<true>, 256, smem, &occ))) return rc;
+        const int grid = std::max(1, std::min((int)((m + 7) / 8), std::max(occ, 1) * h->num_sms));
+        Work wk{nullptr, (int32_t)m, h->cursors + 2 * NBINS};
+        ++g_launches;
+        k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, o, wk, nm_max, (long long)h->tier_flops1);
+        CU(cudaGetLastError());
+        if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st, h->scan_scratch, h->bound_off,
+                                 &h->d_summary->flag, &h->d_summary->total_nnz)))
+            return rc;
+        trace("direct");
+        if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+        if (!h->h_summary->pad) {
+            h->sum = *h->h_summary;
+            mark(h, 1);
+            mark(h, 2);
+            mark(h, 3);
+            h->stats = mm_stats_t{};
+            h->stats.generated_flops = (int64_t)h->sum.gen_flops;
+            h->stats.rows_empty = h->sum.bin_count[BIN_EMPTY];
+            h->stats.rows_push = m - h->stats.rows_empty;
+            h->total_nnz = h->sum.total_nnz;
+            h->stats.evaluated_multiplies = (int64_t)h->sum.evaluated;
+            h->bound_flag = h->sum.flag;
+            for (int b = 0; b < NBINS; b++) h->sum.bin_count[b] = 0;   // profile: every row in one launch
+            h->sum.bin_count[BIN_F64D] = (int)m;
+            mark(h, 4);
+            *out_nnz = h->total_nnz;
+            h->active = true;
+            return MM_OK;
+        }
+        // fall back: clear what the direct pass accumulated, then analyse
+        CU(cudaMemsetAsync(h->d_summary, 0, zero_bytes, st));
     }
+    if ((rc = run_analysis())) return rc;
     // ---- small plain one-phase problems: one pass over every row with a
     // fixed single-warp table, one host sync (no binning round trip).  A row
     // whose mask does not fit sets the overflow flag and the multiply falls
     // back to the binned path below (the analysis summary is already there).
-    const bool tiny = plain_1p && m > 0 && m <= h->tiny_rows && mask->nnz <= h->tiny_nnz &&
+    const bool tiny = !direct && plain_1p && m > 0 && m <= h->tiny_rows && mask->nnz <= h->tiny_nnz &&
                       a->nnz <= h->tiny_nnz &&
                       (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH ||
                        plan->algorithm == MM_ALGO_MSA || plan->algorithm == MM_ALGO_MCA);
-    bool have_summary = false;
     if (tiny) {
         h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
         Out o{};
@@ -1150,6 +1211,23 @@ int mm_multiply_begin(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* 
     return rc;
 }
 
+int mm_multiply(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
+                const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* c_row_ptr, int32_t* c_col_idx,
+                void* c_values, int64_t capacity, int64_t* out_nnz, mm_stats_t* stats) {
+    if (!h || !out_nnz || !c_row_ptr) return fail(MM_ERR_INPUT, "null argument");
+    DeviceGuard dg(h->device);
+    h->user_row_ptr = c_row_ptr;
+    int rc = begin_impl(h, plan, mask, a, b, b_csc, (cudaStream_t)stream, false, nullptr, out_nnz);
+    h->user_row_ptr = nullptr;
+    if (rc) {
+        release(h);
+        return rc;
+    }
+    if (*out_nnz > capacity) return fail(MM_ERR_CAPACITY, "output capacity " + std::to_string(capacity) +
+                                                              " below nnz(C) = " + std::to_string(*out_nnz));
+    return end_impl(h, c_row_ptr, c_col_idx, c_values, stats);
+}
+
 int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_values, mm_stats_t* stats) {
     if (!h) return fail(MM_ERR_INPUT, "null handle");
     DeviceGuard dg(h->device);
@@ -1196,6 +1274,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 11 && params[11] > 0 && params[11] <= 4) h->load_shift_wide = (int)params[11];
     if (n > 12 && params[12] >= 0) h->tiny_rows = params[12];   // 0 disables the single-pass path
     if (n > 13 && params[13] >= 0) h->tiny_nnz = params[13];
+    if (n > 14 && params[14] >= 0) h->direct_on = params[14] != 0;
     return MM_OK;
 }
 

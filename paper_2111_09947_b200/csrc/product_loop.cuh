@@ -77,6 +77,7 @@ struct RowInfo {
 template <int GW>
 struct RowFetcher {
     int n = 0, q = 0;
+    int per = MM_ROWS_PER_FETCH;   // rows per fetch (1-warp groups); 1 when rows are few per warp
     int64_t li = 0, las = 0, lae = 0, lms = 0, lme = 0;
     __device__ __forceinline__ bool next(const Prob& p, const Work& wk, int gt, int bar_id, int* s_row,
                                          RowInfo& ri) {
@@ -84,10 +85,10 @@ struct RowFetcher {
         if (GW == 1) {
             if (q >= n) {
                 int b = 0;
-                if (lane == 0) b = atomicAdd(wk.cursor, MM_ROWS_PER_FETCH);
+                if (lane == 0) b = atomicAdd(wk.cursor, per);
                 b = __shfl_sync(FULL, b, 0);
                 if (b >= wk.count) return false;
-                n = wk.count - b < MM_ROWS_PER_FETCH ? wk.count - b : MM_ROWS_PER_FETCH;
+                n = wk.count - b < per ? wk.count - b : per;
                 q = 0;
                 if (lane < n) {
                     li = wk.rows ? wk.rows[b + lane] : b + lane;   // rows == nullptr: every row in order

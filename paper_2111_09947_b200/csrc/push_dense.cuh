@@ -309,6 +309,7 @@ k_push_dense(Prob p, Out o, Work wk, int words_max) {
     group_bar(bar_id, GT);
     unsigned long long evaluated = 0;
     RowFetcher<GW> rf;
+    if (wk.count < 4 * (int)(gridDim.x * (blockDim.x / (32 * GW)))) rf.per = 1;   // few rows: one per fetch
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
         dense_row<GW, KIND, NUMERIC, COMP>(p, o, cnt, val, words_max, dummy_s, ri, gt, bar_id, s_warp + g * GW, bsm,

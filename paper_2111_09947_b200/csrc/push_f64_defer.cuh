@@ -22,7 +22,8 @@
 //   3. the hits fold into their rank slots in ascending t (each hit's order
 //      among the hits of its slot, then rounds: order 0 stores) — the
 //      reference's ascending-k order, bit for bit;
-//   4. gather in mask order (_kernels.py:78-85, 308-313), reset what was used.
+//   4. the distinct hit slots are the row's entries, emitted in rank order =
+//      mask order (_kernels.py:78-85, 308-313); the filter words are reset.
 //
 // A row with more hits than the list holds is redone with the in-order walk
 // over the same slots, so results never depend on the list capacity.
@@ -163,8 +164,12 @@ __device__ __forceinline__ void defer_walk(const Prob& p, const DeferWarp& w, ui
     }
 }
 
-// Fold the warp's hit list into the rank slots in ascending t per slot.
-__device__ __forceinline__ void defer_fold(int n, const DeferWarp& w, int lane) {
+// Fold the warp's hit list (n hits) into the rank slots in ascending t per
+// slot, then emit the row straight from the list: the distinct slots are the
+// row's output entries, in rank (= mask) order.  Returns the entry count;
+// only the slots used are touched, so nothing proportional to nm remains.
+template <bool NUMERIC>
+__device__ __forceinline__ int defer_fold_emit(int n, const DeferWarp& w, const Out& o, int64_t w0, int lane) {
     constexpr int PER = DEFER_CAP / 32;
     int slot[PER], order[PER];
     double v[PER];
@@ -186,26 +191,48 @@ __device__ __forceinline__ void defer_fold(int n, const DeferWarp& w, int lane) 
         }
     }
     maxr = __reduce_max_sync(FULL, maxr);
-    for (int r = 0; r <= maxr; r++) {
+    if (NUMERIC) {
+        for (int r = 0; r <= maxr; r++) {
 #pragma unroll
-        for (int q = 0; q < PER; q++) {
-            if (slot[q] >= 0 && order[q] == r) {
-                if (r == 0) {
-                    w.vals[slot[q]] = v[q];
-                    w.cnt[slot[q]] = 1;
-                } else {
-                    w.vals[slot[q]] += v[q];
+            for (int q = 0; q < PER; q++) {
+                if (slot[q] >= 0 && order[q] == r) {
+                    if (r == 0) w.vals[slot[q]] = v[q];
+                    else w.vals[slot[q]] += v[q];
                 }
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
+    // output position of a slot = distinct slots below it = order-0 hits below it
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PER; q++)
+        if (q * 32 + lane < n) w.h_t[q * 32 + lane] = order[q];   // reuse: h_t := order
+    __syncwarp();
+    int distinct = 0;
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+        const bool first = slot[q] >= 0 && order[q] == 0;
+        distinct += first;
+        if (NUMERIC && first) {
+            int pos = 0;
+            for (int f = 0; f < n; f++) pos += (w.h_t[f] == 0) & (w.h_rank[f] < slot[q]);
+            o.idx[w0 + pos] = w.mrow[slot[q]];
+            ((double*)o.val)[w0 + pos] = w.vals[slot[q]];
+        }
+    }
+    return (int)warp_sum_ll(distinct);
 }
 
 // One warp per row of one bin (rows fetched dynamically); nm_max: the bin's
 // largest mask row (<= F64D_MAX_NM).
+// Direct mode (flops_cap > 0; wk.rows == nullptr: every row, no analysis
+// pass before it): the kernel also sums generated_flops and the empty rows
+// into o.gen_flops / o.empty_rows, and a row whose mask exceeds nm_max or
+// whose products exceed flops_cap raises o.overflow (the host then runs the
+// binned path instead).
 template <bool NUMERIC>
-__global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work wk, int nm_max) {
+__global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work wk, int nm_max, long long flops_cap) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -215,12 +242,24 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
     for (int e = lane; e < nm_max; e += 32) w.cnt[e] = 0;
     __syncwarp();
     const uint32_t filter_s = (uint32_t)__cvta_generic_to_shared(w.filter);
-    unsigned long long evaluated = 0;
+    unsigned long long evaluated = 0, gen = 0;
+    int empty = 0;
     RowFetcher<1> rf;
+    // few rows per warp: one row per fetch, so no warp serialises several
+    // rows' latency chains while others idle
+    if (wk.count < 4 * (int)(gridDim.x * (blockDim.x >> 5))) rf.per = 1;
     RowInfo ri;
     while (rf.next(p, wk, lane, 0, nullptr, ri)) {
         const int64_t ms = ri.ms;
         const int nm = (int)(ri.me - ms);
+        if (flops_cap && nm > nm_max) {
+            if (lane == 0) {
+                atomicExch(o.overflow, 1);
+                o.row_nnz[ri.i] = 0;
+            }
+            continue;
+        }
+        long long rf_lane = 0;   // direct mode: this lane's share of the row's products
         // 1. mask copy + filter
         for (int r = lane; r < nm; r += 32) {
             const int32_t j = p.m_idx[ms + r];
@@ -249,6 +288,7 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
                 bs = p.b_ptr[k];
                 len = (int)(p.b_ptr[k + 1] - bs);
             }
+            if (sub == 0) rf_lane += len;
             // long B rows: the warp walks them, coalesced, 4 loads in flight
             unsigned longm = __ballot_sync(FULL, sub == 0 && len >= DEFER_LONG);
             while (longm) {
@@ -278,44 +318,57 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
             }
         }
         __syncwarp();
-        // 3. ordered fold (or the in-order walk when the list overflowed)
+        // 3. ordered fold and emit from the hit list, or (list overflow) the
+        // in-order walk into the slots and a gather in mask order
+        if (flops_cap) {
+            const long long rflops = warp_sum_ll(rf_lane);
+            gen += rflops;
+            empty += (rflops == 0 || nm == 0);
+            if (rflops > flops_cap) {
+                if (lane == 0) {
+                    atomicExch(o.overflow, 1);
+                    o.row_nnz[ri.i] = 0;
+                }
+                for (int r = lane; r < nm; r += 32) w.filter[defer_bit(w.mrow[r]) >> 5] = 0u;
+                __syncwarp();
+                continue;
+            }
+        }
+        const int64_t w0 = NUMERIC ? o.off[ri.i] : 0;
+        int running = 0;
         if (nh <= DEFER_CAP) {
             evaluated += ev;
-            if (NUMERIC) {
-                if (nh) defer_fold(nh, w, lane);
-            } else {
-                for (int e = lane; e < nh; e += 32) w.cnt[w.h_rank[e]] = 1;
-            }
+            if (nh) running = defer_fold_emit<NUMERIC>(nh, w, o, w0, lane);
         } else {
             DeferLocatorF64 loc{w, nm};
             evaluated += ordered_products_f64<NUMERIC>(p, loc, ri.as, ri.ae, lane);
-        }
-        __syncwarp();
-        // 4. gather in mask order; reset the slots and the filter words used
-        const int64_t w0 = NUMERIC ? o.off[ri.i] : 0;
-        int running = 0;
-        for (int rb = 0; rb < nm; rb += 32) {
-            const int r = rb + lane;
-            const bool set = r < nm && w.cnt[r] > 0;
-            const unsigned bal = __ballot_sync(FULL, set);
-            if (NUMERIC && set) {
-                const int64_t d = w0 + running + __popc(bal & lanemask_lt());
-                o.idx[d] = w.mrow[r];
-                ((double*)o.val)[d] = w.vals[r];
+            __syncwarp();
+            for (int rb = 0; rb < nm; rb += 32) {
+                const int r = rb + lane;
+                const bool set = r < nm && w.cnt[r] > 0;
+                const unsigned bal = __ballot_sync(FULL, set);
+                if (NUMERIC && set) {
+                    const int64_t d = w0 + running + __popc(bal & lanemask_lt());
+                    o.idx[d] = w.mrow[r];
+                    ((double*)o.val)[d] = w.vals[r];
+                }
+                running += __popc(bal);
             }
-            running += __popc(bal);
+            __syncwarp();
+            for (int r = lane; r < nm; r += 32) w.cnt[r] = 0;
         }
-        __syncwarp();
         if (lane == 0) o.row_nnz[ri.i] = running;
-        for (int r = lane; r < nm; r += 32) {
-            w.cnt[r] = 0;
-            w.filter[defer_bit(w.mrow[r]) >> 5] = 0u;
-        }
+        // reset the filter words of the mask row
+        for (int r = lane; r < nm; r += 32) w.filter[defer_bit(w.mrow[r]) >> 5] = 0u;
         __syncwarp();
     }
     if (NUMERIC) {
         const long long e = warp_sum_ll((long long)evaluated);
         if (lane == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);
+    }
+    if (flops_cap && lane == 0) {
+        if (gen) atomicAdd(o.gen_flops, gen);
+        if (empty) atomicAdd(o.empty_rows, empty);
     }
 }
 

@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(256) k_push_msas(Prob p, Out o, Work wk, int d
     }
     unsigned long long evaluated = 0;
     RowFetcher<GW> rf;
+    if (wk.count < 4 * (int)(gridDim.x * (blockDim.x / (32 * GW)))) rf.per = 1;   // few rows: one per fetch
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
         msas_row<GW, KIND, NUMERIC>(p, o, region, nm_max, d_max, blk_max, ri, gt, bar_id, s_warp + g * GW, bsm,

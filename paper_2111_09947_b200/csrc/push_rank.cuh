@@ -435,6 +435,7 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
         for (int w = gt; w < (SMEM ? msa_words16(words_max) : words_max); w += GT) bits[w] = 0u;
     }
     RowFetcher<GW> rf;
+    if (wk.count < 4 * (int)(gridDim.x * (blockDim.x / (32 * GW)))) rf.per = 1;   // few rows: one per fetch
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri))
         rank_row<GW, KIND, MSA, NUMERIC, SMEM>(p, o, region, nm_max, words_max, dummy_s, ri, gt, bar_id,

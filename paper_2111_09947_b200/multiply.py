@@ -21,6 +21,7 @@ the GPU (the reference guarantees results independent of them).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 import threading
@@ -36,6 +37,9 @@ from .semiring import Semiring, arithmetic_semiring
 from .sparse import CscMatrix, CsrMatrix, MaskView, SparseError, to_csr
 
 ALGORITHMS = ("msa", "hash", "mca", "heap", "heapdot", "inner")
+# plain masks up to this many entries take the one-call multiply into
+# nnz(M)-sized outputs (mm_multiply); larger ones allocate nnz(C) exactly
+ONE_CALL_MAX_NNZ = 1 << 22
 EXTRA_ALGORITHMS = ("auto",)
 PHASES = ("1p", "2p")
 _LABELS = {"msa": "MSA", "hash": "Hash", "mca": "MCA", "heap": "Heap",
@@ -139,7 +143,19 @@ def _raise(rc: int):
     raise RuntimeError(f"CUDA error in maskmul: {msg}")
 
 
+_plan_cache: dict = {}
+
+
 def _plan_t(plan: MultiplyPlan, comp: bool) -> _lib.PlanT:
+    """The C plan struct of (plan, complement flag), built once per distinct plan."""
+    key = (plan, comp)
+    pt = _plan_cache.get(key)
+    if pt is None:
+        pt = _plan_cache[key] = _plan_t_build(plan, comp)
+    return pt
+
+
+def _plan_t_build(plan: MultiplyPlan, comp: bool) -> _lib.PlanT:
     ni = plan.effective_n_inspect
     return _lib.PlanT(_lib.MM_ALGO[plan.algorithm], 2 if plan.phases == "2p" else 1, int(comp),
                       int(plan.semiring.kernel_id),
@@ -166,38 +182,62 @@ def multiply_device(mask: DeviceCsr, a: DeviceCsr, b: DeviceCsr, plan: MultiplyP
         raise PlanError(f"the {'mask-compressed accumulator' if plan.algorithm == 'mca' else 'inner-product algorithm'}"
                         " does not support complemented masks")
     dev = a.idx.device
+    di = dev.index if dev.index is not None else torch.cuda.current_device()
     if stream is None:
-        stream = torch.cuda.current_stream(dev)
+        # the current stream's raw handle (torch.cuda.current_stream builds a
+        # Python Stream object: several microseconds per multiply)
+        raw = torch._C._cuda_getCurrentRawStream(di)
+        on_current = True
+    else:
+        raw = stream.cuda_stream
+        on_current = raw == torch._C._cuda_getCurrentRawStream(di)
     lib = _lib.load()
-    h = _handle(dev.index if dev.index is not None else torch.cuda.current_device())
+    h = _handle(di)
     pt = _plan_t(plan, comp)
     mm_mask, mm_a, mm_b = mask.mm(), a.mm(), b.mm()
     mm_bt = b_csc.mm() if b_csc is not None else None
     nnz = C.c_int64(0)
     dtype = torch.float64 if pt.dtype == _lib.MM_DTYPE_FLOAT64 else torch.int64
     stats = MultiplyStats()
+    st = _lib.StatsT()
     t0 = time.perf_counter()
-    rc = lib.mm_multiply_begin(h, C.byref(pt), C.byref(mm_mask), C.byref(mm_a), C.byref(mm_b),
-                               C.byref(mm_bt) if mm_bt is not None else None,
-                               C.c_void_p(stream.cuda_stream), C.byref(nnz))
-    if rc:
-        _raise(rc)
-    t1 = time.perf_counter()
-    n = int(nnz.value)
-    if stream == torch.cuda.current_stream(dev):
-        row_ptr = torch.empty(mask.nrows + 1, dtype=torch.int64, device=dev)
-        col_idx = torch.empty(n, dtype=torch.int32, device=dev)
-        values = torch.empty(n, dtype=dtype, device=dev)
-    else:
-        with torch.cuda.stream(stream):
+    # C's arrays come from the caching allocator on the multiply's stream
+    ctx = contextlib.nullcontext() if on_current else torch.cuda.stream(stream)
+    with ctx:
+        if not comp and mask.nnz <= ONE_CALL_MAX_NNZ:
+            # plain mask: nnz(C) <= nnz(M) (the one-phase bound, multiply.py:233),
+            # so C's arrays are allocated up front and one call does the whole
+            # multiply (one host sync, compaction queued right after it)
+            cap = mask.nnz
+            row_ptr = torch.empty(mask.nrows + 1, dtype=torch.int64, device=dev)
+            col_idx = torch.empty(cap, dtype=torch.int32, device=dev)
+            values = torch.empty(cap, dtype=dtype, device=dev)
+            rc = lib.mm_multiply(h, C.byref(pt), C.byref(mm_mask), C.byref(mm_a), C.byref(mm_b),
+                                 C.byref(mm_bt) if mm_bt is not None else None, C.c_void_p(raw),
+                                 row_ptr.data_ptr(), col_idx.data_ptr() if cap else None,
+                                 values.data_ptr() if cap else None, cap, C.byref(nnz), C.byref(st))
+            if rc:
+                _raise(rc)
+            t1 = time.perf_counter()
+            n = int(nnz.value)
+            if n < cap:   # shrink in place (the storage stays; no new tensor objects)
+                col_idx.resize_(n)
+                values.resize_(n)
+        else:
+            rc = lib.mm_multiply_begin(h, C.byref(pt), C.byref(mm_mask), C.byref(mm_a), C.byref(mm_b),
+                                       C.byref(mm_bt) if mm_bt is not None else None,
+                                       C.c_void_p(raw), C.byref(nnz))
+            if rc:
+                _raise(rc)
+            t1 = time.perf_counter()
+            n = int(nnz.value)
             row_ptr = torch.empty(mask.nrows + 1, dtype=torch.int64, device=dev)
             col_idx = torch.empty(n, dtype=torch.int32, device=dev)
             values = torch.empty(n, dtype=dtype, device=dev)
-    st = _lib.StatsT()
-    rc = lib.mm_multiply_end(h, row_ptr.data_ptr(), col_idx.data_ptr() if n else None,
-                             values.data_ptr() if n else None, C.byref(st))
-    if rc:
-        _raise(rc)
+            rc = lib.mm_multiply_end(h, row_ptr.data_ptr(), col_idx.data_ptr() if n else None,
+                                     values.data_ptr() if n else None, C.byref(st))
+            if rc:
+                _raise(rc)
     t2 = time.perf_counter()
     if plan.phases == "2p":
         stats.symbolic_seconds, stats.numeric_seconds = t1 - t0, t2 - t1
@@ -334,7 +374,7 @@ def reduce_sum(values: torch.Tensor) -> torch.Tensor:
     dt = _lib.MM_DTYPE_FLOAT64 if values.dtype == torch.float64 else _lib.MM_DTYPE_INT64
     rc = _lib.load().mm_reduce_sum(values.data_ptr() if values.numel() else None, values.numel(),
                                    dt, out.data_ptr(),
-                                   C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+                                   C.c_void_p(torch._C._cuda_getCurrentRawStream(dev.index)))
     if rc:
         _raise(rc)
     return out
