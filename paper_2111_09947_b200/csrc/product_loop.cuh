@@ -7,6 +7,9 @@
 // over the lanes of a group of GW warps.
 #pragma once
 #include "common.cuh"
+#ifdef MM_STAGE_TMA
+#include "stage_tma.cuh"
+#endif
 
 namespace mm {
 
@@ -282,6 +285,12 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
                 const long long b0 = shfl64(sb, src);
                 const int n0 = __shfl_sync(FULL, plen, src);
                 const long long a0 = CARRY ? shfl64(sa, src) : 0;
+#ifdef MM_STAGE_TMA
+                if (n0 >= MM_STAGE_MIN && stage_available()) {
+                    stage_segment(p, pr, b0, n0, a0, lane32);
+                    continue;
+                }
+#endif
                 const int32_t* bp = p.b_idx + b0;
                 int c = 0;
                 for (; c + CH <= n0; c += CH) {   // full chunks: no bounds predicates

@@ -308,6 +308,9 @@ k_push_dense(Prob p, Out o, Work wk, int words_max) {
     }
     group_bar(bar_id, GT);
     unsigned long long evaluated = 0;
+#ifdef MM_STAGE_TMA
+    stage_init();
+#endif
     RowFetcher<GW> rf;
     if (wk.count < 4 * (int)(gridDim.x * (blockDim.x / (32 * GW)))) rf.per = 1;   // few rows: one per fetch
     RowInfo ri;

@@ -804,6 +804,9 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
     BatchSmem bsm = bind_batch<GW, KIND>(bbase);
     unsigned char* wq = smem + (SMEM ? (size_t)groups * cap_max * HashEntry<KIND>::bytes : 0) +
                         (size_t)groups * BATCH_BYTES + (size_t)(threadIdx.x >> 5) * queue_bytes<KIND>();
+#ifdef MM_STAGE_TMA
+    stage_init();
+#endif
     Table<KIND> tb;
     tb.bind(base, cap_max);
     __shared__ uint32_t s_dummy[(GW == 32 ? 32 : (GW == 16 ? 16 : 8)) * 32];

@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(256) k_push_msas(Prob p, Out o, Work wk, int d
         for (int q = gt; q < 32 * blk_max; q += GT) words[q] = 0u;
     }
     unsigned long long evaluated = 0;
+#ifdef MM_STAGE_TMA
+    stage_init();
+#endif
     RowFetcher<GW> rf;
     if (wk.count < 4 * (int)(gridDim.x * (blockDim.x / (32 * GW)))) rf.per = 1;   // few rows: one per fetch
     RowInfo ri;

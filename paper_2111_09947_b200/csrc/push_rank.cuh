@@ -429,6 +429,9 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
     BatchSmem bsm = bind_batch<GW, KIND>(bbase);
     __shared__ uint32_t s_dummy[(GW == 32 ? 32 : (GW == 16 ? 16 : 8)) * 32];
     const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(s_dummy + threadIdx.x);
+#ifdef MM_STAGE_TMA
+    stage_init();
+#endif
     unsigned long long evaluated = 0;
     if (MSA) {
         uint32_t* bits = (uint32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)nm_max) + 4 * (size_t)nm_max);
