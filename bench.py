@@ -41,14 +41,14 @@ sys.path.insert(0, ROOT)
 METRIC = "masked-SpGEMM useful GFLOP/s & triangles/s; HBM GB/s vs roofline at 1/2/4/8 B200"
 UNIT = "useful GFLOP/s"
 EXPECTED_TRIANGLES = {20: 423909251}
-NBINS = 47          # analyze.cuh Bin::NBINS
+NBINS = 48          # analyze.cuh Bin::NBINS
 SUMMARY_BYTES = 32 + NBINS * 8 + NBINS * 4 * 4 + 16          # sizeof(mm::Summary), read back twice per multiply
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
 BIN_NAMES = (["empty"] + [f"{m}_t{t}{c}" for m in ("plain", "ctab", "csrch")
                           for t, c in ((0, "s"), (0, "l"), (1, "s"), (1, "l"), (2, "s"), (2, "l"), (3, "g"))]
              + ["pull"] + [f"{f}_t{t}" for f in ("msa", "mca", "heap") for t in range(4)] + ["single"]
              + [f"msa_sparse_t{t}" for t in range(3)] + [f"msa_dense_t{t}" for t in range(3)]
-             + [f"msa_dense_comp_t{t}" for t in range(3)] + ["pull_lane", "f64_defer"])
+             + [f"msa_dense_comp_t{t}" for t in range(3)] + ["pull_lane", "f64_defer", "msa_window"])
 assert len(BIN_NAMES) == NBINS
 
 

@@ -35,7 +35,8 @@ enum Bin : int {
     BIN_MSADC0 = 42,  // + tier (0..2): complemented MSA over every column (narrow outputs)
     BIN_PULL_LANE = 45,  // pull, one lane per mask entry (short masks, short A rows and B columns)
     BIN_F64D = 46,       // ordered float64, plain hash with deferred hits (push_f64_defer.cuh)
-    NBINS = 47
+    BIN_MSAW = 47,       // MSA plan, plain order-free rows too wide for the shared tiers: windowed MSA (push_rank.cuh)
+    NBINS = 48
 };
 __host__ __device__ constexpr bool is_msadc_bin(int b) { return b >= BIN_MSADC0 && b < BIN_MSADC0 + 3; }
 __host__ __device__ constexpr bool is_msas_bin(int b) { return b >= BIN_MSAS0 && b < BIN_MSAS0 + 3; }
@@ -206,6 +207,8 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
     if (!ap.comp && (fam == FAM_MSA || fam == FAM_MCA)) {
         const int64_t bytes = fam == FAM_MSA ? msa_bytes(words, nm, kind) : mca_bytes(nm, kind);
         const int tier = bytes <= ap.rank_budget[tf] ? tf : 3;
+        // MSA rows past the shared tiers: shared-memory windows, not a global bitmap
+        if (fam == FAM_MSA && tier == 3 && !ap.ordered) return BIN_MSAW;
         return (fam == FAM_MSA ? BIN_MSA0 : BIN_MCA0) + tier;
     }
     // hash family (and the complement forms of MSA / heap)

@@ -23,6 +23,7 @@ struct Prob {
     const int32_t* bt_idx;
     const void* bt_val;
     const int64_t* row_flops;
+    int64_t cursor_stride;   // sliced hub rows: int64 slice cursors per group (entries), 0 = none
     int64_t nrows;
     int64_t ncols;
 };
@@ -123,6 +124,23 @@ __device__ __forceinline__ int64_t lower_bound_range(const int32_t* __restrict__
         else hi = mid;
     }
     return lo;
+}
+
+// first position in idx[lo, hi) whose value is >= key, galloping from lo:
+// O(log(distance)) loads, one when the answer is lo (sliced hub rows walk
+// every B row slice by slice, each slice starting where the previous ended).
+__device__ __forceinline__ int64_t gallop_lower_bound(const int32_t* __restrict__ idx, int64_t lo, int64_t hi,
+                                                      int32_t key) {
+    if (lo >= hi || idx[lo] >= key) return lo;
+    int64_t step = 1;
+    int64_t prev = lo;   // idx[prev] < key
+    for (;;) {
+        const int64_t q = prev + step;
+        if (q >= hi) return lower_bound_range(idx, prev + 1, hi, key);
+        if (idx[q] >= key) return lower_bound_range(idx, prev + 1, q, key);
+        prev = q;
+        step <<= 1;
+    }
 }
 
 // lower_bound over a sorted int32 array.

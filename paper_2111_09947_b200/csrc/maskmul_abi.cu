@@ -194,6 +194,7 @@ struct mm_handle {
     int64_t tiny_rows = 1 << 15, tiny_nnz = 1 << 20;   // single-pass path for small plain 1P multiplies
     bool direct_on = true;                              // direct path for ordered float64 (see begin_impl)
     int64_t* user_row_ptr = nullptr;                    // mm_multiply: C's row pointer, written by the scan
+    bool slice_cursors = true;                          // sliced hub rows resume each B row per slice
     // ---- concurrent bin launches ----
     static constexpr int NAUX = 3;
     cudaStream_t aux[NAUX] = {};
@@ -538,16 +539,24 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             if ((rc = kernel_occupancy((const void*)kern, threads, smem, &occ))) return rc;
             int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
             unsigned char* gslab = nullptr;
+            Prob pq = h->prob;
             if (!smem_table) {
                 size_t bytes = (size_t)grid * groups * table;
                 CU(cudaMallocAsync((void**)&gslab, bytes, st));
+                h->allocs.push_back(gslab);
+            } else if (sliced && h->slice_cursors) {
+                // per-group slice cursors (one int64 per A entry of the row,
+                // at most 1 GiB in all; wider rows search every slice)
+                const int64_t per_group = ((int64_t)1 << 30) / (8 * (int64_t)grid * groups);
+                pq.cursor_stride = std::min<int64_t>(std::max(h->sum.max_na, 1), per_group);
+                CU(cudaMallocAsync((void**)&gslab, (size_t)grid * groups * pq.cursor_stride * 8, st));
                 h->allocs.push_back(gslab);
             }
             ++g_launches;
             if (debug_launches())
                 fprintf(stderr, "[mm] hash bin %d rows %d gw %d threads %d cap_lg %d smem %zu grid %d occ %d\n", b,
                         cnt, gw, threads, cap_lg, smem, grid, occ);
-            kern<<<grid, threads, smem, st>>>(h->prob, out, wk, h->row_cap_lg, cap_lg, gslab);
+            kern<<<grid, threads, smem, st>>>(pq, out, wk, h->row_cap_lg, cap_lg, gslab);
             CU(cudaGetLastError());
             continue;
         }
@@ -580,6 +589,34 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
                 fprintf(stderr, "[mm] rank bin %d rows %d gw %d threads %d words %d nm %d smem %zu grid %d occ %d\n", b,
                         cnt, gw, threads, words_max, nm_max, smem, grid, occ);
             kern<<<grid, threads, smem, st>>>(h->prob, out, wk, words_max, nm_max, gslab);
+            CU(cudaGetLastError());
+            continue;
+        }
+        if (b == BIN_MSAW) {
+            // windowed MSA (hub rows): one 16-warp group per block, per-group
+            // slice cursors in a global slab
+            const int kind = numeric ? h->kind : 0;
+            void (*kern)(Prob, Out, Work, unsigned char*) = nullptr;
+            if (!numeric) kern = k_push_msaw<0, false>;
+            else if (kind == 0) kern = k_push_msaw<0, true>;
+            else if (kind == 1) kern = k_push_msaw<1, true>;
+            else return fail(MM_ERR_INTERNAL, "windowed MSA bin with ordered float64 rows");
+            const size_t smem = ((msaw_region_bytes(kind) + 15) & ~(size_t)15) + batch_bytes_rt(MSAW_GW, kind);
+            int occ = 0;
+            if ((rc = kernel_occupancy((const void*)kern, MSAW_GW * 32, smem, &occ))) return rc;
+            const int grid = std::max(1, std::min(cnt, std::max(occ, 1) * h->num_sms));
+            Prob pq = h->prob;
+            unsigned char* gslab = nullptr;
+            if (h->slice_cursors) {
+                const int64_t per_group = ((int64_t)1 << 30) / (8 * (int64_t)grid);
+                pq.cursor_stride = std::min<int64_t>(std::max(h->sum.max_na, 1), per_group);
+                CU(cudaMallocAsync((void**)&gslab, (size_t)grid * pq.cursor_stride * 8, st));
+                h->allocs.push_back(gslab);
+            }
+            ++g_launches;
+            if (debug_launches())
+                fprintf(stderr, "[mm] msa-window bin rows %d smem %zu grid %d occ %d\n", cnt, smem, grid, occ);
+            kern<<<grid, MSAW_GW * 32, smem, st>>>(pq, out, wk, gslab);
             CU(cudaGetLastError());
             continue;
         }
@@ -1275,6 +1312,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 12 && params[12] >= 0) h->tiny_rows = params[12];   // 0 disables the single-pass path
     if (n > 13 && params[13] >= 0) h->tiny_nnz = params[13];
     if (n > 14 && params[14] >= 0) h->direct_on = params[14] != 0;
+    if (n > 15 && params[15] >= 0) h->slice_cursors = params[15] != 0;
     return MM_OK;
 }
 

@@ -202,16 +202,23 @@ __device__ __forceinline__ void tail_chunk(const Prob& p, PR& pr, const int32_t*
 #ifndef MM_SEARCH_U
 #define MM_SEARCH_U 2
 #endif
+//   cur (column-range mode over consecutive ranges of one row): cur[t - as]
+//   holds where A entry t's B row reached at the end of the previous range,
+//   so a range starts there (no search) and ends by a galloping search.
 template <int GW, int KIND, class PR, bool SEARCH = false>
 __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as, int64_t ae, int gt,
                                               int bar_id, int* s_warp, BatchSmem bsm,
                                               int32_t c_lo = INT32_MIN, int32_t c_hi = INT32_MAX,
-                                              const int32_t* srch_m = nullptr, int64_t srch_nm = 0) {
+                                              const int32_t* srch_m = nullptr, int64_t srch_nm = 0,
+                                              int64_t* cur = nullptr) {
     constexpr int GT = GW * 32;
 #ifndef MM_PRODUCT_UNROLL
 #define MM_PRODUCT_UNROLL 4
 #endif
-    constexpr int U = MM_PRODUCT_UNROLL;   // independent B loads in flight per lane
+#ifndef MM_WIDE_UNROLL
+#define MM_WIDE_UNROLL 8   // 16/32-warp groups: more loads in flight (cfg5 424 -> 406 ms)
+#endif
+    constexpr int U = GW >= 16 ? MM_WIDE_UNROLL : MM_PRODUCT_UNROLL;   // independent B loads in flight per lane
     constexpr int CH = 32 * U;
     constexpr int NB = GT;
     constexpr bool CARRY = carries_a(KIND);
@@ -224,8 +231,16 @@ __device__ __forceinline__ void flat_products(const Prob& p, PR& pr, int64_t as,
             const int32_t k = p.a_idx[t];
             base = p.b_ptr[k];
             int64_t end = p.b_ptr[k + 1];
-            if (c_lo != INT32_MIN) base = lower_bound_range(p.b_idx, base, end, c_lo);
-            if (c_hi != INT32_MAX) end = lower_bound_range(p.b_idx, base, end, c_hi);
+            if (cur) {
+                if (c_lo != INT32_MIN) base = cur[t - as];
+                if (c_hi != INT32_MAX) {
+                    end = gallop_lower_bound(p.b_idx, base, end, c_hi);
+                    cur[t - as] = end;
+                }
+            } else {
+                if (c_lo != INT32_MIN) base = lower_bound_range(p.b_idx, base, end, c_lo);
+                if (c_hi != INT32_MAX) end = lower_bound_range(p.b_idx, base, end, c_hi);
+            }
             len = (int)(end - base);
             if (KIND == 1) av = ((const long long*)p.a_val)[t];
             if (KIND == 3) av = t;

@@ -445,7 +445,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
                                          int64_t ms, int64_t me, int32_t c_lo, int32_t c_hi, int64_t w_base,
                                          int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
                                          BatchSmem bsm, unsigned char* wq, uint32_t dummy_s,
-                                         unsigned long long& evaluated) {
+                                         unsigned long long& evaluated, int64_t* cur = nullptr) {
     constexpr int GT = GW * 32;
     // Plain masks in shared memory keep the table clean between rows (each
     // row cleans what it touched) and first look for a multiplier that puts
@@ -580,7 +580,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.b_val = p.b_val;
         pr.evaluated = 0;
         flat_products<GW, KIND, decltype(pr), MODE == MODE_PLAIN && MM_SEARCH_ON>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi,
-                                                                               p.m_idx + ms, nm);
+                                                                               p.m_idx + ms, nm, cur);
         evaluated += pr.evaluated;
     } else if (CLEAN && pl.hm == 2) {
         DirectProber<KIND, NUMERIC, 2> pr;
@@ -595,7 +595,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.b_val = p.b_val;
         pr.evaluated = 0;
         flat_products<GW, KIND, decltype(pr), MODE == MODE_PLAIN && MM_SEARCH_ON>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi,
-                                                                               p.m_idx + ms, nm);
+                                                                               p.m_idx + ms, nm, cur);
         evaluated += pr.evaluated;
     } else {
         WarpProber<KIND, MODE, NUMERIC, SMEM> pr;
@@ -614,7 +614,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
         pr.lane = lane;
         pr.evaluated = 0;
         flat_products<GW, KIND, decltype(pr), MODE == MODE_PLAIN && MM_SEARCH_ON>(p, pr, as, ae, gt, bar_id, s_warp, bsm, c_lo, c_hi,
-                                                                               p.m_idx + ms, nm);
+                                                                               p.m_idx + ms, nm, cur);
         evaluated += pr.evaluated;
     }
     group_bar(bar_id, GT);
@@ -747,7 +747,7 @@ template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
                                          int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
                                          BatchSmem bsm, unsigned char* wq, uint32_t dummy_s,
-                                         unsigned long long& evaluated) {
+                                         unsigned long long& evaluated, int64_t* cur = nullptr) {
     constexpr bool CLEAN = MODE == MODE_PLAIN && SMEM && KIND != 2;
     const int64_t nm = ri.me - ri.ms;
     const int64_t w = NUMERIC ? o.off[ri.i] : 0;
@@ -766,9 +766,11 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
             const int64_t s1 = s0 + slice < ri.me ? s0 + slice : ri.me;
             const int32_t c_lo = s0 == ri.ms ? INT32_MIN : p.m_idx[s0];
             const int32_t c_hi = s1 < ri.me ? p.m_idx[s1] : INT32_MAX;
+            // slice cursors: each A entry's B row resumes where the previous slice ended
             total += hash_part<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, s0, s1, c_lo, c_hi, w + total,
                                                               cap_lg_max, cap_lg_max, gt, bar_id, s_warp, bsm,
-                                                              wq, dummy_s, evaluated);
+                                                              wq, dummy_s, evaluated,
+                                                              ri.ae - ri.as <= p.cursor_stride ? cur : nullptr);
         }
     }
     if (gt == 0) o.row_nnz[ri.i] = total;
@@ -783,7 +785,10 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
 #define MM_HASH_MINB 4   // <= 64 registers: 4 blocks of 256 threads per SM (5 spills; measured on cfg2)
 #endif
 template <int GW, bool SMEM, int KIND, int MODE, bool NUMERIC>
-__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256), GW <= 8 ? MM_HASH_MINB : (GW == 16 ? 2 : 1))
+#ifndef MM_HASH16_MINB
+#define MM_HASH16_MINB 2
+#endif
+__global__ void __launch_bounds__(GW == 32 ? 1024 : (GW == 16 ? 512 : 256), GW <= 8 ? MM_HASH_MINB : (GW == 16 ? MM_HASH16_MINB : 1))
 k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
             unsigned char* gslab) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -809,6 +814,10 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
 #endif
     Table<KIND> tb;
     tb.bind(base, cap_max);
+    // shared-memory tables: gslab, when given, holds the sliced rows' cursors
+    int64_t* cursors = SMEM && gslab && p.cursor_stride
+                           ? (int64_t*)gslab + ((size_t)blockIdx.x * groups + g) * (size_t)p.cursor_stride
+                           : nullptr;
     __shared__ uint32_t s_dummy[(GW == 32 ? 32 : (GW == 16 ? 16 : 8)) * 32];
     const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(s_dummy + threadIdx.x);
     if (MODE == MODE_PLAIN && SMEM && KIND != 2) {   // hash_row keeps it clean from here on
@@ -842,7 +851,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
         }
         hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg ? row_cap_lg[ri.i] : cap_lg_max,
                                                 cap_lg_max, gt, bar_id, s_warp + g * GW, bsm, wq, dummy_s,
-                                                evaluated);
+                                                evaluated, cursors);
     }
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);

@@ -450,3 +450,132 @@ k_push_rank(Prob p, Out o, Work wk, int words_max, int nm_max, unsigned char* gs
 }
 
 }  // namespace mm
+
+namespace mm {
+
+// ---------------------------------------------------------------------------
+// Windowed MSA for hub rows (plain masks, order-free kinds): the mask row is
+// cut into column windows whose packed bitmap (16 columns + 16-bit rank per
+// word) and rank slots fit a fixed shared-memory region; each window keeps
+// only the products whose column falls inside it (each B row's sub-range,
+// resumed from a per-A-entry cursor), so a 163,558-entry mask row runs in
+// ~30 windows with the one-load MSA probe.  Reference semantics: MSA
+// (_kernels.py:30-87) restricted to a column range per pass; windows run in
+// column order and append, so C stays in mask order.
+// ---------------------------------------------------------------------------
+constexpr int MSAW_GW = 16;
+constexpr int MSAW_WORDS = 8192;   // packed words per window (131,072 columns)
+constexpr int MSAW_SLOTS = 6144;   // mask entries per window
+
+__host__ __device__ constexpr size_t msaw_region_bytes(int kind) {
+    return (size_t)(kind == 0 ? 0 : 8) * MSAW_SLOTS + 4 * (size_t)MSAW_SLOTS + 4 * (size_t)(MSAW_WORDS + 4);
+}
+
+template <int KIND, bool NUMERIC>
+__global__ void __launch_bounds__(MSAW_GW * 32, 2) k_push_msaw(Prob p, Out o, Work wk, unsigned char* gslab) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_row[1];
+    __shared__ int s_warp[MSAW_GW];
+    __shared__ int s_r1;
+    constexpr int GT = MSAW_GW * 32;
+    const int gt = threadIdx.x;
+    const int bar_id = 1;
+    unsigned char* region = smem;
+    unsigned long long* val = (unsigned long long*)region;                     // KIND 1
+    int32_t* cnt = (int32_t*)(region + (KIND == 0 ? 0 : 8 * (size_t)MSAW_SLOTS));
+    uint32_t* words = (uint32_t*)(cnt + MSAW_SLOTS);
+    BatchSmem bsm = bind_batch<MSAW_GW, KIND>(smem + ((msaw_region_bytes(KIND) + 15) & ~(size_t)15));
+    __shared__ uint32_t s_dummy[GT];
+    const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(s_dummy + threadIdx.x);
+    int64_t* cur = gslab && p.cursor_stride ? (int64_t*)gslab + (size_t)blockIdx.x * (size_t)p.cursor_stride : nullptr;
+    for (int w = gt; w < MSAW_WORDS + 4; w += GT) words[w] = 0u;
+    group_bar(bar_id, GT);
+    unsigned long long evaluated = 0;
+    RowFetcher<MSAW_GW> rf;
+    RowInfo ri;
+    while (rf.next(p, wk, gt, bar_id, s_row, ri)) {
+        const int64_t ms = ri.ms, nm = ri.me - ri.ms;
+        const int64_t w0 = NUMERIC ? o.off[ri.i] : 0;
+        int64_t* rcur = ri.ae - ri.as <= p.cursor_stride ? cur : nullptr;
+        int64_t total = 0;
+        for (int64_t r0 = 0; r0 < nm;) {
+            const int32_t lo = p.m_idx[ms + r0] & ~15;
+            if (gt == 0) {
+                // the window: mask entries with column < lo + 16 * (MSAW_WORDS - 1), at most MSAW_SLOTS
+                const int64_t cap = nm - r0 < MSAW_SLOTS ? nm - r0 : MSAW_SLOTS;
+                const int64_t lim = (int64_t)lo + 16ll * (MSAW_WORDS - 1);
+                int64_t n = cap;
+                if ((int64_t)p.m_idx[ms + r0 + cap - 1] >= lim)
+                    n = lower_bound_range(p.m_idx, ms + r0, ms + r0 + cap, (int32_t)lim) - (ms + r0);
+                s_r1 = (int)(n > 0 ? n : 1);
+            }
+            group_bar(bar_id, GT);
+            const int ns = s_r1;
+            group_bar(bar_id, GT);
+            const int64_t r1 = r0 + ns;
+            const int32_t hi = p.m_idx[ms + r1 - 1];
+            // 1. clear slots, 2. mark the window's mask entries
+            for (int r = gt; r < ns; r += GT) {
+                cnt[r] = 0;
+                if (KIND == 1) val[r] = 0ull;
+            }
+            group_bar(bar_id, GT);
+            for (int r = gt; r < ns; r += GT) {
+                const int32_t j = p.m_idx[ms + r0 + r];
+                const uint32_t off = (uint32_t)(j - lo);
+                const uint32_t w = off >> 4;
+                const bool first = r == 0 || (((uint32_t)(p.m_idx[ms + r0 + r - 1] - lo)) >> 4) != w;
+                atomicOr(words + w, (1u << (off & 15u)) | (first ? (uint32_t)r << 16 : 0u));
+            }
+            group_bar(bar_id, GT);
+            // 3. products whose column lies in the window's range
+            const int32_t c_lo = r0 == 0 ? INT32_MIN : p.m_idx[ms + r0];
+            const int32_t c_hi = r1 < nm ? p.m_idx[ms + r1] : INT32_MAX;
+            MsaProber<KIND, NUMERIC> pr;
+            pr.bits_s = (uint32_t)__cvta_generic_to_shared(words);
+            pr.cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+            pr.val_s = KIND == 0 ? 0u : (uint32_t)__cvta_generic_to_shared(val);
+            pr.lo = lo;
+            pr.guard = (((uint32_t)(hi - lo) >> 4) + 1) << 4;
+            pr.dummy_s = dummy_s;
+            pr.b_val = p.b_val;
+            pr.evaluated = 0u;
+            flat_products<MSAW_GW, KIND>(p, pr, ri.as, ri.ae, gt, bar_id, s_warp, bsm, c_lo, c_hi, nullptr, 0,
+                                         rcur);
+            evaluated += pr.evaluated;
+            group_bar(bar_id, GT);
+            // 4. gather the window in mask order, appended to the row
+            int running = 0;
+            for (int rb = 0; rb < ns; rb += GT) {
+                const int r = rb + gt;
+                const bool set = r < ns && cnt[r] > 0;
+                if (KIND == 0 && NUMERIC && set) evaluated += (unsigned)cnt[r];
+                int tot;
+                const int pos = group_prefix<MSAW_GW>(set, &tot, s_warp, bar_id, gt);
+                if (NUMERIC && set) {
+                    const int64_t d = w0 + total + running + pos;
+                    o.idx[d] = p.m_idx[ms + r0 + r];
+                    if (KIND == 0) {
+                        if (o.out_f64) ((double*)o.val)[d] = (double)cnt[r];
+                        else ((long long*)o.val)[d] = cnt[r];
+                    } else {
+                        ((unsigned long long*)o.val)[d] = val[r];
+                    }
+                }
+                running += tot;
+            }
+            total += running;
+            // 5. leave the bitmap all-zero
+            for (int r = gt; r < ns; r += GT) words[((uint32_t)(p.m_idx[ms + r0 + r] - lo)) >> 4] = 0u;
+            group_bar(bar_id, GT);
+            r0 = r1;
+        }
+        if (gt == 0) o.row_nnz[ri.i] = total;
+    }
+    if (NUMERIC) {
+        const long long e = warp_sum_ll((long long)evaluated);
+        if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);
+    }
+}
+
+}  // namespace mm
