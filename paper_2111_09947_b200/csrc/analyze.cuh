@@ -154,9 +154,11 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             int64_t w = 4 + ap.vbytes;
             int64_t push = 16 * na + flops * w;
             int64_t pull = 16 * nm + (nm * na + pull_cols) * w;
-            if (ap.has_bt && pull < push) fam = FAM_PULL;
-            // ordered float64 single-warp rows with short masks: the direct /
-            // cuckoo hash probe with hits folded in k order afterwards
+            // ordered float64 rows push through the deferred-hit kernel at a
+            // fraction of the in-order walk's cost: pull must win by 1.5x
+            if (ap.has_bt && (ap.ordered ? pull + (pull >> 1) : pull) < push) fam = FAM_PULL;
+            // ordered float64 single-warp rows with short masks: the deferred-hit
+            // kernel (mask filter, hits folded in k order afterwards)
             else if (ap.ordered && tf == 0 && nm <= F64D_MAX_NM) return f64d_bin(nm, cap_lg_out);
             // ordered float64 rows (one warp, k order): the rank search beats
             // both the bitmap and the hash for short mask rows

@@ -923,7 +923,12 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     // generated flops itself, and flags rows it cannot take (mask row over
     // F64D_MAX_NM, products over the 4-warp tier bound); one host sync.  A
     // flagged multiply continues on the binned path below.
-    const bool direct = plain_1p && h->kind == 2 && m > 0 && !use_bt && h->direct_on &&
+    // with B^T (auto), only when the average pull cost per mask entry does not
+    // undercut push by 1.5x (the per-row push/pull model needs the analysis)
+    const double est_push = (double)a->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->nrows, 1));
+    const double est_pull = (double)mask->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->ncols, 1) +
+                                                 (double)a->nnz / (double)std::max<int64_t>(m, 1));
+    const bool direct = plain_1p && h->kind == 2 && m > 0 && h->direct_on && (!use_bt || 1.5 * est_pull >= est_push) &&
                         (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH);
     bool have_summary = false;
     if (direct) {

@@ -512,3 +512,42 @@ def test_concurrent_threads_share_no_handle():
     assert not errs, errs
     for c in out:
         assert torch.equal(c.idx, ref.idx) and torch.equal(c.values, ref.values)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_float64_push_pull_per_row_with_bt(seed):
+    """Ordered float64 rows given B^T (auto): the deferred-hit kernel picks
+    push or pull per row (push_f64_defer.cuh), both fold in ascending k, so C
+    is bitwise the oracle's.  Rows span short / wide masks (pull vs push),
+    dense hits (hit-list overflow -> in-order walk), masks over the direct
+    path's limit (fallback to the binned path) and 1P / 2P."""
+    rng = np.random.default_rng(4242 + seed)
+    n = 3000
+    blocks = []
+    for rows, da, dm in ((200, 8, 1), (200, 8, 4), (200, 16, 64), (50, 30, 300), (20, 60, 3000)):
+        blocks.append((random_csr(rng, rows, n, da), random_csr(rng, rows, n, dm)))
+    a = from_arrays(sum(x.nrows for x, _ in blocks), n,
+                    np.concatenate([np.repeat(np.arange(x.nrows), np.diff(x.row_ptr)) + off
+                                    for (x, _), off in zip(blocks, np.cumsum([0] + [x.nrows for x, _ in blocks[:-1]]))]),
+                    np.concatenate([x.col_idx[: x.nnz] for x, _ in blocks]),
+                    rng.standard_normal(sum(x.nnz for x, _ in blocks)))
+    m = from_arrays(a.nrows, n,
+                    np.concatenate([np.repeat(np.arange(y.nrows), np.diff(y.row_ptr)) + off
+                                    for (_, y), off in zip(blocks, np.cumsum([0] + [y.nrows for _, y in blocks[:-1]]))]),
+                    np.concatenate([y.col_idx[: y.nnz] for _, y in blocks]),
+                    np.ones(sum(y.nnz for _, y in blocks)))
+    b = random_csr(rng, n, n, 6).astype(np.float64)
+    b.values[:] = rng.standard_normal(b.nnz)
+    sem = arithmetic_semiring(np.float64)
+    r = oracle.masked_multiply(m.pattern(), a, b, semiring_id=0, dtype=np.float64)
+    want = digest_csr(r.row_ptr, r.col_idx, r.values)
+    da = DeviceCsr.from_host(a, dtype=np.float64)
+    db = DeviceCsr.from_host(b, dtype=np.float64)
+    dm = DeviceCsr.from_host(m.pattern(), with_values=False)
+    bt = db.transpose_storage()
+    for ph in ("1p", "2p"):
+        for algo, csc in (("auto", bt), ("auto", None), ("hash", None), ("inner", bt)):
+            c, st = multiply_device(dm, da, db, MultiplyPlan(algorithm=algo, phases=ph, semiring=sem), b_csc=csc)
+            assert _digest(c.to_host()) == want, (algo, ph, csc is not None)
+            assert st.evaluated_multiplies == r.evaluated_multiplies
+            assert st.generated_flops == r.generated_flops
