@@ -155,8 +155,9 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
             int64_t push = 16 * na + flops * w;
             int64_t pull = 16 * nm + (nm * na + pull_cols) * w;
             // ordered float64 rows push through the deferred-hit kernel at a
-            // fraction of the in-order walk's cost: pull must win by 1.5x
-            if (ap.has_bt && (ap.ordered ? pull + (pull >> 1) : pull) < push) fam = FAM_PULL;
+            // fraction of the in-order walk's cost: pull must win by 2.5x
+            // (cfg3: d1 rows pull, d4 / d16 / d64 rows push)
+            if (ap.has_bt && (ap.ordered ? (5 * pull) >> 1 : pull) < push) fam = FAM_PULL;
             // ordered float64 single-warp rows with short masks: the deferred-hit
             // kernel (mask filter, hits folded in k order afterwards)
             else if (ap.ordered && tf == 0 && nm <= F64D_MAX_NM) return f64d_bin(nm, cap_lg_out);

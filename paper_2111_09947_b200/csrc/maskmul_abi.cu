@@ -921,14 +921,14 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     // ---- direct path for ordered float64 plain one-phase multiplies: no
     // analysis pass — the deferred-hit kernel takes every row, sums the
     // generated flops itself, and flags rows it cannot take (mask row over
-    // F64D_MAX_NM, products over the 4-warp tier bound); one host sync.  A
+    // 128 entries, products over the 4-warp tier bound); one host sync.  A
     // flagged multiply continues on the binned path below.
     // with B^T (auto), only when the average pull cost per mask entry does not
-    // undercut push by 1.5x (the per-row push/pull model needs the analysis)
+    // undercut push by 3x (the per-row push/pull model needs the analysis)
     const double est_push = (double)a->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->nrows, 1));
     const double est_pull = (double)mask->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->ncols, 1) +
                                                  (double)a->nnz / (double)std::max<int64_t>(m, 1));
-    const bool direct = plain_1p && h->kind == 2 && m > 0 && h->direct_on && (!use_bt || 1.5 * est_pull >= est_push) &&
+    const bool direct = plain_1p && h->kind == 2 && m > 0 && h->direct_on && (!use_bt || 3.0 * est_pull >= est_push) &&
                         (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH);
     bool have_summary = false;
     if (direct) {
@@ -943,7 +943,9 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
         o.overflow = &h->d_summary->pad;
         o.gen_flops = &h->d_summary->gen_flops;
         o.empty_rows = &h->d_summary->bin_count[BIN_EMPTY];
-        const int nm_max = (int)F64D_MAX_NM;
+        // mask rows up to 128 entries (wider ones fall back): 8 warps x 6 KB,
+        // four blocks per SM
+        const int nm_max = 128;
         const size_t smem = 8 * defer_warp_bytes(nm_max);
         int occ = 0;
         if ((rc = kernel_occupancy((const void*)k_push_f64_defer<true>, 256, smem, &occ))) return rc;

@@ -280,13 +280,14 @@ def _prepare(mask, a, b, plan: MultiplyPlan, device=None):
     b_csr = to_csr(b) if is_csc else b
     db = DeviceCsr.from_host(b_csr, dtype=dt, device=device, with_values=need_vals)
     dbt = None
-    if plan.algorithm == "inner" or (plan.algorithm == "auto" and (is_csc or (not comp and _pull_pays(mask, a, b_csr)))):
+    ordered = plan.semiring.kernel_id == 0 and dt.kind == "f"
+    if plan.algorithm == "inner" or (plan.algorithm == "auto" and (is_csc or (not comp and _pull_pays(mask, a, b_csr, ordered)))):
         dbt = (DeviceCsr.from_host(b, dtype=dt, device=device, with_values=need_vals)
                if is_csc else db.transpose_storage())
     return dm, da, db, dbt, comp
 
 
-def _pull_pays(mask, a, b) -> bool:
+def _pull_pays(mask, a, b, ordered: bool = False) -> bool:
     """auto: build B^T in the (untimed) preparation when the byte model of
     SURVEY §8(d) makes pull clearly cheaper in aggregate — the mask is much
     sparser than the product space (cfg3 d1 / d4).  The per-row choice is
@@ -303,7 +304,10 @@ def _pull_pays(mask, a, b) -> bool:
     nnz_b = int(b.row_ptr[-1])
     col_len = np.bincount(np.asarray(b.col_idx[:nnz_b], dtype=np.int64), minlength=b.shape[1])
     pull = int((na * nm).sum()) + int(col_len[np.asarray(mask.col_idx[:nnz_m], dtype=np.int64)].sum())
-    return 3 * pull < 2 * flops
+    # float64 plus-times rows push through the deferred-hit kernel at a third
+    # of the pull path's cost per probe (the device's per-row model weighs the
+    # same way, analyze.cuh classify_row)
+    return (3 if ordered else 1.5) * pull < flops
 
 
 def masked_multiply_with_stats(mask, a, b, plan: MultiplyPlan, device=None):
