@@ -34,8 +34,17 @@ for r in rows[2:]:
                  "ncu_ms": val(r, "gpu__time_duration.sum")})
 rd = sum(k["dram_read_bytes"] for k in kern)
 wr = sum(k["dram_write_bytes"] for k in kern)
+import subprocess
+try:
+    commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True).stdout.strip()
+except Exception:
+    commit = None
 json.dump({"source": "ncu --set full --clock-control none capture of one cfg2 multiply "
                      "(tools/profile_step.py --reps 1, algorithm=auto), numeric-phase kernels k_push*/k_pull*",
+           "commit": sys.argv[3] if len(sys.argv) > 3 else commit,
+           "config": "cfg2: R-MAT s20 ef16, L = tril(relabel(G)), C = L.(L L) plus-pair int64, auto",
+           "command": "ncu --set full --clock-control none -k regex:'k_push|k_pull' --csv --page raw "
+                      "python tools/profile_step.py --reps 1",
            "numeric_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
            "ncu_ms_sum": sum(k["ncu_ms"] for k in kern), "kernels": kern},
           open(out, "w"), indent=1)
