@@ -44,11 +44,7 @@ EXPECTED_TRIANGLES = {20: 423909251}
 NBINS = 48          # analyze.cuh Bin::NBINS
 SUMMARY_BYTES = 32 + NBINS * 8 + NBINS * 4 * 4 + 16          # sizeof(mm::Summary), read back twice per multiply
 L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
-BIN_NAMES = (["empty"] + [f"{m}_t{t}{c}" for m in ("plain", "ctab", "csrch")
-                          for t, c in ((0, "s"), (0, "l"), (1, "s"), (1, "l"), (2, "s"), (2, "l"), (3, "g"))]
-             + ["pull"] + [f"{f}_t{t}" for f in ("msa", "mca", "heap") for t in range(4)] + ["single"]
-             + [f"msa_sparse_t{t}" for t in range(3)] + [f"msa_dense_t{t}" for t in range(3)]
-             + [f"msa_dense_comp_t{t}" for t in range(3)] + ["pull_lane", "f64_defer", "msa_window"])
+from paper_2111_09947_b200.multiply import BIN_NAMES  # noqa: E402  (kernel bin names)
 assert len(BIN_NAMES) == NBINS
 
 

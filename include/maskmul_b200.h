@@ -112,7 +112,10 @@ int mm_destroy(mm_handle_t* h);
  *     fills *stats.  Returns MM_ERR_INTERNAL if the reference's assertions
  *     (multiply.py:375,390) would fail.
  *
- * b: B as CSR (required: push kernels and flops_per_row read it).
+ * b: B as CSR (required: push kernels and flops_per_row read it; for
+ *   MM_ALGO_INNER only its row pointer is read — idx / values may be NULL,
+ *   as the reference's _Prepared holds B only as CSC for inner,
+ *   multiply.py:205-210).
  * b_csc: B^T storage (CSC) for the pull path; required when
  *   plan->algorithm is MM_ALGO_INNER, optional for MM_ALGO_AUTO (without it
  *   AUTO runs push only), ignored otherwise.

@@ -188,8 +188,6 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         *aux_out = na;
         return BIN_HEAP0 + 3;
     }
-    // the hash plan's ordered single-warp plain rows: same deferred form
-    if (fam == FAM_HASH && ap.ordered && !ap.comp && tf == 0 && nm <= F64D_MAX_NM) return f64d_bin(nm, cap_lg_out);
     const bool single_ok = !ap.ordered || tf == 0;
     if (!ap.comp && fam == FAM_MSA && single_ok && msa_bytes(words, nm, kind) > ap.rank_budget[tr] &&
         msas_bytes(words, nm, kind) <= ap.rank_budget[tr] && nm < 65536) {

@@ -308,7 +308,10 @@ int validate(const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* 
         return fail(MM_ERR_INPUT, "nnz of A, B and the mask must be in [0, 2^31)");
     if ((a->nnz && (!a->ptr || !a->idx)) || !a->ptr || !b->ptr || !mask->ptr)
         return fail(MM_ERR_INPUT, "missing index arrays");
-    if (plan->semiring == MM_SR_ARITHMETIC && ((a->nnz && !a->values) || (b->nnz && !b->values)))
+    // inner reads B only through B^T (B may be its row pointer alone, as the
+    // reference's _Prepared holds B as CSC for inner, multiply.py:205-210)
+    if (plan->semiring == MM_SR_ARITHMETIC &&
+        ((a->nnz && !a->values) || (plan->algorithm != MM_ALGO_INNER && b->nnz && !b->values)))
         return fail(MM_ERR_INPUT, "plus-times needs operand values");
     if (plan->algorithm == MM_ALGO_INNER) {
         if (!bt || !bt->ptr) return fail(MM_ERR_INPUT, "the inner-product algorithm needs B in CSC form");
@@ -929,7 +932,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     const double est_pull = (double)mask->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->ncols, 1) +
                                                  (double)a->nnz / (double)std::max<int64_t>(m, 1));
     const bool direct = plain_1p && h->kind == 2 && m > 0 && h->direct_on && (!use_bt || 3.0 * est_pull >= est_push) &&
-                        (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH);
+                        plan->algorithm == MM_ALGO_AUTO;
     bool have_summary = false;
     if (direct) {
         h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
@@ -986,10 +989,9 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     // fixed single-warp table, one host sync (no binning round trip).  A row
     // whose mask does not fit sets the overflow flag and the multiply falls
     // back to the binned path below (the analysis summary is already there).
+    // (a hash accumulator: only the plans that name one, or leave the choice)
     const bool tiny = !direct && plain_1p && m > 0 && m <= h->tiny_rows && mask->nnz <= h->tiny_nnz &&
-                      a->nnz <= h->tiny_nnz &&
-                      (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH ||
-                       plan->algorithm == MM_ALGO_MSA || plan->algorithm == MM_ALGO_MCA);
+                      a->nnz <= h->tiny_nnz && (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH);
     if (tiny) {
         h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
         Out o{};
@@ -1031,6 +1033,12 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
             h->total_nnz = h->sum.total_nnz;
             h->stats.evaluated_multiplies = (int64_t)h->sum.evaluated;
             h->bound_flag = h->sum.flag;
+            // profile: every non-empty row ran the 1-warp plain hash kernel
+            for (int b = 1; b < NBINS; b++) {
+                h->sum.bin_flops[hash_bin(MODE_PLAIN, 0, 0)] += b == hash_bin(MODE_PLAIN, 0, 0) ? 0 : h->sum.bin_flops[b];
+                h->sum.bin_count[hash_bin(MODE_PLAIN, 0, 0)] += b == hash_bin(MODE_PLAIN, 0, 0) ? 0 : h->sum.bin_count[b];
+                if (b != hash_bin(MODE_PLAIN, 0, 0)) h->sum.bin_count[b] = 0, h->sum.bin_flops[b] = 0;
+            }
             trace("sync2");
             mark(h, 4);
             *out_nnz = h->total_nnz;

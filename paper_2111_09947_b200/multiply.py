@@ -371,6 +371,24 @@ def flops_of(a, b, device=None) -> int:
     return int(tot.item())
 
 
+def last_kernel_rows(device=None) -> dict:
+    """Rows per kernel bin of this thread's last multiply on `device` (bin
+    names as in DESIGN.md §4: which accumulator computed how many rows)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    nb = 64
+    rows = (C.c_int64 * nb)()
+    n = _lib.load().mm_profile_bins(_handle(dev.index), rows, None, nb)
+    return {BIN_NAMES[b]: int(rows[b]) for b in range(min(n, len(BIN_NAMES))) if rows[b]}
+
+
+# kernel bins (csrc/analyze.cuh enum Bin), named for last_kernel_rows / bench.py
+BIN_NAMES = (["empty"] + [f"hash_{m}_t{t}{c}" for m in ("plain", "ctab", "csrch")
+                          for t, c in ((0, "s"), (0, "l"), (1, "s"), (1, "l"), (2, "s"), (2, "l"), (3, "g"))]
+             + ["pull"] + [f"{f}_t{t}" for f in ("msa", "mca", "heap") for t in range(4)] + ["single"]
+             + [f"msa_sparse_t{t}" for t in range(3)] + [f"msa_dense_t{t}" for t in range(3)]
+             + [f"msa_dense_comp_t{t}" for t in range(3)] + ["pull_lane", "f64_defer", "msa_window"])
+
+
 def reduce_sum(values: torch.Tensor) -> torch.Tensor:
     """Deterministic device sum (the triangle-count reduction, graphs.py:96)."""
     dev = values.device

@@ -551,3 +551,33 @@ def test_float64_push_pull_per_row_with_bt(seed):
             assert _digest(c.to_host()) == want, (algo, ph, csc is not None)
             assert st.evaluated_multiplies == r.evaluated_multiplies
             assert st.generated_flops == r.generated_flops
+
+
+def test_plan_runs_its_accumulator():
+    """The plan label names the accumulator that runs: every
+    non-empty row of a named plan lands in a kernel of that family.  The one
+    documented substitution: complemented MSA rows whose output is too wide
+    for a state per column in shared memory run the hash complement kernels
+    (DESIGN.md §4)."""
+    from paper_2111_09947_b200.multiply import last_kernel_rows
+    rng = np.random.default_rng(77)
+    fam = {"msa": ("msa_",), "mca": ("mca_",), "heap": ("heap_",), "heapdot": ("heap_",),
+           "hash": ("hash_",), "inner": ("pull",)}
+    for rows, da, dm, n in ((200, 4, 6, 500), (40, 30, 120, 40000), (8, 200, 900, 40000), (3, 600, 9000, 40000)):
+        a = random_csr(rng, rows, 2000, da)
+        b = random_csr(rng, 2000, n, 4)
+        m = random_csr(rng, rows, n, dm)
+        for sem in (SR, plus_pair_semiring(np.int64), arithmetic_semiring(np.float64)):
+            aa, bb = a, b
+            if sem.dtype == np.float64:
+                aa = a.astype(np.float64)
+                bb = b.astype(np.float64)
+            for comp in (False, True):
+                for algo, prefixes in fam.items():
+                    if comp and algo in ("mca", "inner"):
+                        continue
+                    masked_multiply(m.pattern(), aa, bb, MultiplyPlan(algorithm=algo, complemented=comp, semiring=sem))
+                    used = {k: v for k, v in last_kernel_rows().items() if k != "empty"}
+                    allowed = prefixes + (("hash_ctab", "hash_csrch") if comp and algo == "msa" else ())
+                    bad = [k for k in used if not k.startswith(allowed)]
+                    assert not bad, (algo, comp, sem.name, str(sem.dtype), used)
