@@ -92,6 +92,7 @@ struct AnalyzeParams {
     int pair;        // plus-pair (4-byte table values)
     int vbytes;      // value bytes read per operand entry (0 plus-pair, 8 otherwise)
     int has_bt;      // B^T (CSC) available
+    const int64_t* done;   // rows with done[i] >= 0 were computed already (direct pass): skipped
 };
 
 __host__ __device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
@@ -291,6 +292,10 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
     for (int64_t r0 = warp * 32; r0 < p.nrows; r0 += nwarps * 32) {
         const int64_t i = r0 + lane;
         bool live = i < p.nrows;
+        if (live && ap.done && ap.done[i] >= 0) {   // computed by the direct pass
+            live = false;
+            row_bin[i] = (uint8_t)BIN_EMPTY;
+        }
         int64_t as = 0, ae = 0, ms = 0, me = 0;
         if (live) {
             as = p.a_ptr[i];

@@ -859,6 +859,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     ap.pair = pair;
     ap.vbytes = pair ? 0 : 8;
     ap.has_bt = use_bt;
+    ap.done = nullptr;
     const int64_t m = h->nrows;
 
     // One pool allocation carves every per-multiply array; summary and fetch
@@ -923,9 +924,9 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     };
     // ---- direct path for ordered float64 plain one-phase multiplies: no
     // analysis pass — the deferred-hit kernel takes every row, sums the
-    // generated flops itself, and flags rows it cannot take (mask row over
-    // 128 entries, products over the 4-warp tier bound); one host sync.  A
-    // flagged multiply continues on the binned path below.
+    // generated flops itself, and leaves rows it cannot take (mask row over
+    // 128 entries, products over the 1-warp tier bound) marked; one host
+    // sync.  Marked rows then run on the binned path below.
     // with B^T (auto), only when the average pull cost per mask entry does not
     // undercut push by 3x (the per-row push/pull model needs the analysis)
     const double est_push = (double)a->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->nrows, 1));
@@ -955,7 +956,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
         const int grid = std::max(1, std::min((int)((m + 7) / 8), std::max(occ, 1) * h->num_sms));
         Work wk{nullptr, (int32_t)m, h->cursors + 2 * NBINS};
         ++g_launches;
-        k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, o, wk, nm_max, (long long)h->tier_flops1);
+        k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, o, wk, nm_max, (long long)h->tier_flops0);
         CU(cudaGetLastError());
         if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st, h->scan_scratch, h->bound_off,
                                  &h->d_summary->flag, &h->d_summary->total_nnz)))
@@ -981,8 +982,12 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
             h->active = true;
             return MM_OK;
         }
-        // fall back: clear what the direct pass accumulated, then analyse
-        CU(cudaMemsetAsync(h->d_summary, 0, zero_bytes, st));
+        // rows the direct pass could not take (row_nnz = -1) go through the
+        // binned path; its rows stay done (the analysis skips them, their
+        // flops / evaluated / empty counts are already in the summary)
+        CU(cudaMemsetAsync(&h->d_summary->flag, 0, 2 * sizeof(int), st));          // flag, pad
+        CU(cudaMemsetAsync(h->cursors, 0, (3 * NBINS + 4) * sizeof(int32_t), st));  // fetch cursors, long rows
+        ap.done = h->row_nnz;
     }
     if ((rc = run_analysis())) return rc;
     // ---- small plain one-phase problems: one pass over every row with a

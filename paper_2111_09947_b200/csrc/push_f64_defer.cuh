@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
         if (flops_cap && nm > nm_max) {
             if (lane == 0) {
                 atomicExch(o.overflow, 1);
-                o.row_nnz[ri.i] = 0;
+                o.row_nnz[ri.i] = -1;   // left to the binned pass
             }
             continue;
         }
@@ -289,6 +289,9 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
                 len = (int)(p.b_ptr[k + 1] - bs);
             }
             if (sub == 0) rf_lane += len;
+            // direct mode: an empty mask row (never launched by the binned path)
+            // only has its flops counted
+            if (nm == 0) continue;
             // long B rows: the warp walks them, coalesced, 4 loads in flight
             unsigned longm = __ballot_sync(FULL, sub == 0 && len >= DEFER_LONG);
             while (longm) {
@@ -322,12 +325,14 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
         // in-order walk into the slots and a gather in mask order
         if (flops_cap) {
             const long long rflops = warp_sum_ll(rf_lane);
-            gen += rflops;
-            empty += (rflops == 0 || nm == 0);
+            if (rflops <= flops_cap) {   // rows left to the binned pass are counted there
+                gen += rflops;
+                empty += (rflops == 0 || nm == 0);
+            }
             if (rflops > flops_cap) {
                 if (lane == 0) {
                     atomicExch(o.overflow, 1);
-                    o.row_nnz[ri.i] = 0;
+                    o.row_nnz[ri.i] = -1;   // left to the binned pass
                 }
                 for (int r = lane; r < nm; r += 32) w.filter[defer_bit(w.mrow[r]) >> 5] = 0u;
                 __syncwarp();
