@@ -161,7 +161,9 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
  * params[12] / params[13] = row / nnz limits of the single-pass small-problem
  * path (32768 / 2^20; 0 disables it), params[14] = 0 disables the direct
  * path of ordered float64 plain one-phase multiplies (no analysis pass),
- * params[15] = 0 disables the slice cursors of sliced hub rows. */
+ * params[15] = 0 disables the slice cursors of sliced hub rows,
+ * params[16] = 0 runs one-phase plain sliced hub rows slice after slice in one
+ * group instead of as (row, slice) work items. */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

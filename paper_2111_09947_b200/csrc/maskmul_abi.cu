@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "pull_inner.cuh"
 #include "push_hash.cuh"
+#include "push_hash_items.cuh"
 #include "push_rank.cuh"
 #include "push_heap.cuh"
 #include "push_single.cuh"
@@ -195,6 +196,11 @@ struct mm_handle {
     bool direct_on = true;                              // direct path for ordered float64 (see begin_impl)
     int64_t* user_row_ptr = nullptr;                    // mm_multiply: C's row pointer, written by the scan
     bool slice_cursors = true;                          // sliced hub rows resume each B row per slice
+    bool split_slices = true;                           // 1P plain sliced rows: (row, slice) work items
+    int32_t* early_idx = nullptr;                       // mm_multiply, small plain 1P: C's arrays, compacted
+    void* early_val = nullptr;                          //   before the single host sync
+    bool compacted = false;
+    int64_t mask_nnz = 0;
     // ---- concurrent bin launches ----
     static constexpr int NAUX = 3;
     cudaStream_t aux[NAUX] = {};
@@ -458,6 +464,45 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
     return launch_bins_on(h, numeric, out, order, n);
 }
 
+// Sliced hub rows of a one-phase plain multiply as (row, slice) items
+// (push_hash_items.cuh): item list, the items kernel, the join.
+int launch_slice_items(mm_handle* h, const Out& out, const Work& wk, int kind, int cap_lg, size_t smem,
+                       cudaStream_t st) {
+    const int64_t slice = (int64_t)MM_SLICE_EIGHTHS << (cap_lg - 3);
+    const int64_t max_items = (int64_t)wk.count + (h->mask_nnz + slice - 1) / slice;
+    if (max_items >= (1ll << 31)) return fail(MM_ERR_INTERNAL, "too many slice items");
+    int32_t* buf = nullptr;
+    const size_t words = (size_t)(wk.count + 1) + 3 * (size_t)max_items + 2;
+    CU(cudaMallocAsync((void**)&buf, words * sizeof(int32_t), st));
+    h->allocs.push_back(buf);
+    int32_t* row_base = buf;
+    int32_t* item_q = row_base + wk.count + 1;
+    int32_t* item_s = item_q + max_items;
+    int32_t* slice_cnt = item_s + max_items;
+    int32_t* ctl = slice_cnt + max_items;   // [0] items, [1] fetch cursor
+    CU(cudaMemsetAsync(ctl, 0, 2 * sizeof(int32_t), st));
+    ++g_launches;
+    k_slice_items<<<1, 1024, 0, st>>>(h->prob, wk, slice, row_base, item_q, item_s, ctl, max_items);
+    CU(cudaGetLastError());
+    void (*kern)(Prob, Out, Work, const int32_t*, const int32_t*, const int32_t*, int32_t*, int64_t, int,
+                 const int32_t*, int32_t*) = kind == 0 ? k_push_hash_items<0> : k_push_hash_items<1>;
+    int occ = 0, rc;
+    if ((rc = kernel_occupancy((const void*)kern, ITEM_GW * 32, smem, &occ))) return rc;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(max_items, (int64_t)std::max(occ, 1) * h->num_sms));
+    ++g_launches;
+    if (debug_launches())
+        fprintf(stderr, "[mm] sliced items rows %d max_items %lld cap_lg %d smem %zu grid %d occ %d\n", wk.count,
+                (long long)max_items, cap_lg, smem, grid, occ);
+    kern<<<grid, ITEM_GW * 32, smem, st>>>(h->prob, out, wk, item_q, item_s, ctl, ctl + 1, slice, cap_lg, row_base,
+                                           slice_cnt);
+    CU(cudaGetLastError());
+    ++g_launches;
+    k_slice_join<<<wk.count, 512, 0, st>>>(wk, out.off, h->prob.m_ptr, slice, row_base, slice_cnt, out.idx,
+                                          (unsigned long long*)out.val, out.row_nnz);
+    CU(cudaGetLastError());
+    return MM_OK;
+}
+
 int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order, int norder) {
     cudaStream_t main_st = h->stream;
     // small multiplies: forking costs more host time than the overlap saves
@@ -538,6 +583,10 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             size_t queue = kind == 2 ? 0 : (size_t)64 * (kind == 1 ? 24 : 8);
             size_t smem = (smem_table ? groups * table : 0) + groups * batch + (threads / 32) * queue;
             if (smem > 227 * 1024) return fail(MM_ERR_INTERNAL, "hash tier table exceeds shared memory");
+            if (sliced && numeric && h->split_slices && h->plan.phases == 1 && !h->plan.complemented) {
+                if ((rc = launch_slice_items(h, out, wk, kind, cap_lg, smem, st))) return rc;
+                continue;
+            }
             int occ = 0;
             if ((rc = kernel_occupancy((const void*)kern, threads, smem, &occ))) return rc;
             int grid = std::max(1, std::min((cnt + groups - 1) / groups, std::max(occ, 1) * h->num_sms));
@@ -810,6 +859,29 @@ int sync_read(mm_handle* h, void* dst, const void* src, size_t bytes) {
     return MM_OK;
 }
 
+// mm_multiply on a small plain one-phase problem: C's arrays are known before
+// nnz(C) is, so the compaction (thread per row: every row fits one slot range)
+// is queued right behind the scan and the summary readback is the only sync.
+// A row the single pass could not take (fallback) only leaves stale C entries,
+// which the fallback's own compaction overwrites.
+int early_compact(mm_handle* h, cudaStream_t st) {
+    const int64_t m = h->nrows;
+    if (!h->early_idx || m <= 0 || m > h->tiny_rows) return MM_OK;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
+    ++g_launches;
+    if (h->out_f64)
+        k_compact_rowwise<double><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
+                                                        (const double*)h->tmp_val, h->c_row_ptr, h->early_idx,
+                                                        (double*)h->early_val, nullptr);
+    else
+        k_compact_rowwise<long long><<<grid, 256, 0, st>>>(m, h->bound_off, h->row_nnz, h->tmp_idx,
+                                                           (const long long*)h->tmp_val, h->c_row_ptr, h->early_idx,
+                                                           (long long*)h->early_val, nullptr);
+    CU(cudaGetLastError());
+    h->compacted = true;
+    return MM_OK;
+}
+
 int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
                const mm_matrix_t* b, const mm_matrix_t* bt, cudaStream_t st, bool symbolic_only,
                int64_t* counts_out, int64_t* out_nnz) {
@@ -818,6 +890,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     if (rc) return rc;
     if (h->active) release(h);
     h->stream = st;
+    h->compacted = false;
     h->launch_base = g_launches;
     mark(h, 0);
     h->plan = *plan;
@@ -866,6 +939,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     // cursors sit together at the front so a single memset clears both.
     const bool need_bound = comp && plan->phases == 1 && !symbolic_only;
     const bool plain_1p = !comp && plan->phases == 1 && !symbolic_only;
+    h->mask_nnz = mask->nnz;
     const int64_t scan_elems = scan_scratch_elems(m);
     size_t off = 0;
     auto carve = [&](size_t bytes) { size_t at = off; off += (bytes + 255) & ~(size_t)255; return at; };
@@ -962,6 +1036,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
                                  &h->d_summary->flag, &h->d_summary->total_nnz)))
             return rc;
         trace("direct");
+        if ((rc = early_compact(h, st))) return rc;
         if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
         if (!h->h_summary->pad) {
             h->sum = *h->h_summary;
@@ -982,6 +1057,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
             h->active = true;
             return MM_OK;
         }
+        h->compacted = false;
         // rows the direct pass could not take (row_nnz = -1) go through the
         // binned path; its rows stay done (the analysis skips them, their
         // flops / evaluated / empty counts are already in the summary)
@@ -1024,6 +1100,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
                                  &h->d_summary->flag, &h->d_summary->total_nnz)))
             return rc;
         trace("tiny");
+        if ((rc = early_compact(h, st))) return rc;
         if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
         have_summary = true;
         if (!h->h_summary->pad) {
@@ -1050,6 +1127,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
             h->active = true;
             return MM_OK;
         }
+        h->compacted = false;
         // fallback: forget what the single pass accumulated
         CU(cudaMemsetAsync(&h->d_summary->evaluated, 0, sizeof(h->d_summary->evaluated), st));
         CU(cudaMemsetAsync(h->cursors + 2 * NBINS, 0, NBINS * sizeof(int32_t), st));
@@ -1146,7 +1224,9 @@ int end_impl(mm_handle* h, int64_t* c_row_ptr, int32_t* c_col_idx, void* c_value
     if (c_row_ptr && c_row_ptr != h->c_row_ptr)
         CU(cudaMemcpyAsync(c_row_ptr, h->c_row_ptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     int* flag = &h->d_summary->flag;
-    if (h->plan.phases == 1) {
+    if (h->plan.phases == 1 && h->compacted) {
+        mark(h, 5);   // compacted before the summary readback (early_compact)
+    } else if (h->plan.phases == 1) {
         if (m > 0 && h->total_nnz <= 2 * m) {
             // sparse outputs: a thread per row
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
@@ -1274,8 +1354,14 @@ int mm_multiply(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, 
     if (!h || !out_nnz || !c_row_ptr) return fail(MM_ERR_INPUT, "null argument");
     DeviceGuard dg(h->device);
     h->user_row_ptr = c_row_ptr;
+    const bool early = plan && mask && !plan->complemented && plan->phases == 1 && capacity >= mask->nnz &&
+                       c_col_idx && c_values;
+    h->early_idx = early ? c_col_idx : nullptr;
+    h->early_val = early ? c_values : nullptr;
     int rc = begin_impl(h, plan, mask, a, b, b_csc, (cudaStream_t)stream, false, nullptr, out_nnz);
     h->user_row_ptr = nullptr;
+    h->early_idx = nullptr;
+    h->early_val = nullptr;
     if (rc) {
         release(h);
         return rc;
@@ -1333,6 +1419,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 13 && params[13] >= 0) h->tiny_nnz = params[13];
     if (n > 14 && params[14] >= 0) h->direct_on = params[14] != 0;
     if (n > 15 && params[15] >= 0) h->slice_cursors = params[15] != 0;
+    if (n > 16 && params[16] >= 0) h->split_slices = params[16] != 0;
     return MM_OK;
 }
 
