@@ -163,7 +163,10 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
  * path of ordered float64 plain one-phase multiplies (no analysis pass),
  * params[15] = 0 disables the slice cursors of sliced hub rows,
  * params[16] = 0 runs one-phase plain sliced hub rows slice after slice in one
- * group instead of as (row, slice) work items. */
+ * group instead of as (row, slice) work items,
+ * params[17] / params[18] = row / nnz limits of the one-launch path for the
+ * smallest plain one-phase multiplies (8192 / 2^17; 0 disables it): the row
+ * kernel's last block scans, compacts and reports through mapped host memory. */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -201,6 +202,12 @@ struct mm_handle {
     void* early_val = nullptr;                          //   before the single host sync
     bool compacted = false;
     int64_t mask_nnz = 0;
+    // ---- fused tail (fused_tail.cuh): one-launch small plain 1P multiplies ----
+    unsigned* d_done = nullptr;          // device ticket counter, zero between multiplies
+    TailResult* h_tail = nullptr;        // mapped pinned host memory the last block writes
+    unsigned long long tail_seq = 0;
+    cudaStream_t tail_stream = nullptr;  // stream of the last fused multiply (the host does not wait for its kernel to retire)
+    int64_t fused_rows = 1 << 13, fused_nnz = 1 << 17;   // one block does the tail: small problems only (0 disables)
     // ---- concurrent bin launches ----
     static constexpr int NAUX = 3;
     cudaStream_t aux[NAUX] = {};
@@ -698,7 +705,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             if (debug_launches())
                 fprintf(stderr, "[mm] f64-defer bin rows %d nm_max %d smem %zu grid %d occ %d\n", cnt, nm_max, smem,
                         grid, occ);
-            k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max, 0ll);
+            k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, out, wk, nm_max, 0ll, Tail{});
             CU(cudaGetLastError());
             continue;
         }
@@ -859,6 +866,62 @@ int sync_read(mm_handle* h, void* dst, const void* src, size_t bytes) {
     return MM_OK;
 }
 
+// Fused tail (fused_tail.cuh): arguments of one multiply, and the host's wait
+// for the last block's counters in mapped memory (a spin on the sequence
+// word; past 2 ms the stream is synchronised, which also surfaces faults).
+Tail make_tail(mm_handle* h) {
+    Tail t{};
+    t.done = h->d_done;
+    t.nrows = h->nrows;
+    t.row_nnz = h->row_nnz;
+    t.slot_off = h->bound_off;
+    t.tmp_idx = h->tmp_idx;
+    t.tmp_val = h->tmp_val;
+    t.c_row_ptr = h->c_row_ptr;
+    t.c_idx = h->early_idx;
+    t.c_val = h->early_val;
+    t.summary = h->d_summary;
+    t.host = h->h_tail;
+    t.seq = ++h->tail_seq;
+    return t;
+}
+
+int wait_tail(mm_handle* h, cudaStream_t st, unsigned long long seq) {
+    volatile unsigned long long* p = &h->h_tail->seq;
+    h->tail_stream = st;
+    const auto t0 = std::chrono::steady_clock::now();
+    int spins = 0;
+    while (*p != seq) {
+        if ((++spins & 63) == 0 &&
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() > 2000.0) {
+            CU(cudaStreamSynchronize(st));
+            if (*p != seq) return fail(MM_ERR_INTERNAL, "fused tail did not report");
+            break;
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    // the rest of the multiply reads the counters from the pinned summary
+    const TailResult r = *h->h_tail;
+#ifdef MM_TAIL_DEBUG
+    if (host_trace())
+        fprintf(stderr, "[mm tail] A %.1f B %.1f C1 %.1f C2 %.1f us, report %.1f us, fence %.1f us, spins %d\n",
+                (r.dbg[4] - r.dbg[0]) * 1e-3, (r.dbg[5] - r.dbg[4]) * 1e-3, (r.dbg[6] - r.dbg[5]) * 1e-3,
+                (r.dbg[1] - r.dbg[6]) * 1e-3, (r.dbg[2] - r.dbg[1]) * 1e-3, (r.dbg[3] - r.dbg[2]) * 1e-3, spins);
+#endif
+    std::memset(h->h_summary, 0, sizeof(Summary));
+    h->h_summary->gen_flops = r.gen_flops;
+    h->h_summary->evaluated = r.evaluated;
+    h->h_summary->total_nnz = r.total_nnz;
+    h->h_summary->bin_count[BIN_EMPTY] = r.empty_rows;
+    h->h_summary->pad = r.overflow;
+    h->h_summary->flag = r.bound_flag;
+    return MM_OK;
+}
+
+bool use_fused_tail(const mm_handle* h, int64_t m, int64_t mask_nnz) {
+    return h->d_done && h->h_tail && h->fused_rows > 0 && m <= h->fused_rows && mask_nnz <= h->fused_nnz;
+}
+
 // mm_multiply on a small plain one-phase problem: C's arrays are known before
 // nnz(C) is, so the compaction (thread per row: every row fits one slot range)
 // is queued right behind the scan and the summary readback is the only sync.
@@ -889,6 +952,12 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     int rc = validate(plan, mask, a, b, bt);
     if (rc) return rc;
     if (h->active) release(h);
+    if (h->tail_stream && h->tail_stream != st) {
+        // the previous fused multiply returned before its kernel retired: its
+        // ticket reset must land before another stream's multiply starts
+        CU(cudaStreamSynchronize(h->tail_stream));
+    }
+    h->tail_stream = nullptr;
     h->stream = st;
     h->compacted = false;
     h->launch_base = g_launches;
@@ -1030,14 +1099,28 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
         const int grid = std::max(1, std::min((int)((m + 7) / 8), std::max(occ, 1) * h->num_sms));
         Work wk{nullptr, (int32_t)m, h->cursors + 2 * NBINS};
         ++g_launches;
-        k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, o, wk, nm_max, (long long)h->tier_flops0);
-        CU(cudaGetLastError());
-        if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st, h->scan_scratch, h->bound_off,
-                                 &h->d_summary->flag, &h->d_summary->total_nnz)))
-            return rc;
-        trace("direct");
-        if ((rc = early_compact(h, st))) return rc;
-        if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+        if (use_fused_tail(h, m, mask->nnz)) {
+            // one launch: the last block scans, compacts and reports (fused_tail.cuh)
+            const size_t fsmem = std::max(smem, tail_smem_bytes());
+            if ((rc = kernel_occupancy((const void*)k_push_f64_defer<true, true>, 256, fsmem, &occ))) return rc;
+            const int fgrid = std::max(1, std::min((int)((m + 7) / 8), std::max(occ, 1) * h->num_sms));
+            const Tail tail = make_tail(h);
+            k_push_f64_defer<true, true><<<fgrid, 256, fsmem, st>>>(h->prob, o, wk, nm_max, (long long)h->tier_flops0,
+                                                                  tail);
+            CU(cudaGetLastError());
+            trace("direct1");
+            if ((rc = wait_tail(h, st, tail.seq))) return rc;
+            h->compacted = h->early_idx != nullptr && !h->h_summary->pad;
+        } else {
+            k_push_f64_defer<true><<<grid, 256, smem, st>>>(h->prob, o, wk, nm_max, (long long)h->tier_flops0, Tail{});
+            CU(cudaGetLastError());
+            if ((rc = exclusive_scan(h->row_nnz, m, h->c_row_ptr, st, h->scan_scratch, h->bound_off,
+                                     &h->d_summary->flag, &h->d_summary->total_nnz)))
+                return rc;
+            trace("direct");
+            if ((rc = early_compact(h, st))) return rc;
+            if ((rc = sync_read(h, h->h_summary, h->d_summary, sizeof(Summary)))) return rc;
+        }
         if (!h->h_summary->pad) {
             h->sum = *h->h_summary;
             mark(h, 1);
@@ -1065,14 +1148,74 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
         CU(cudaMemsetAsync(h->cursors, 0, (3 * NBINS + 4) * sizeof(int32_t), st));  // fetch cursors, long rows
         ap.done = h->row_nnz;
     }
+    // ---- the smallest plain one-phase problems: ONE launch (k_tiny_hash: the
+    // 1-warp hash kernel over every row, flops summed by the kernel, then the
+    // fused tail: scan, compaction, counters into mapped host memory).
+    const bool tiny_ok = !direct && plain_1p && m > 0 && m <= h->tiny_rows && mask->nnz <= h->tiny_nnz &&
+                         a->nnz <= h->tiny_nnz && (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH);
+    bool fused_overflow = false;
+    if (tiny_ok && use_fused_tail(h, m, mask->nnz) && a->nnz <= h->fused_nnz) {
+        h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
+        Out o{};
+        o.off = h->bound_off;
+        o.idx = h->tmp_idx;
+        o.val = h->tmp_val;
+        o.row_nnz = h->row_nnz;
+        o.evaluated = &h->d_summary->evaluated;
+        o.out_f64 = h->out_f64;
+        o.overflow = &h->d_summary->pad;
+        o.gen_flops = &h->d_summary->gen_flops;
+        o.empty_rows = &h->d_summary->bin_count[BIN_EMPTY];
+        void (*kern)(Prob, Out, Work, int, Tail) =
+            h->kind == 0 ? k_tiny_hash<0> : (h->kind == 1 ? k_tiny_hash<1> : k_tiny_hash<2>);
+        const int cap_lg = h->kind == 0 ? 10 : 9;
+        const size_t ebytes = h->kind == 0 ? 8 : 16;
+        const size_t queue = h->kind == 2 ? 0 : (size_t)64 * (h->kind == 1 ? 24 : 8);
+        const size_t smem = std::max(8 * (((size_t)1 << cap_lg) * ebytes + batch_bytes_rt(1, h->kind)) + 8 * queue,
+                                     tail_smem_bytes());
+        int occ = 0;
+        if ((rc = kernel_occupancy((const void*)kern, 256, smem, &occ))) return rc;
+        const int grid = std::max(1, std::min((int)((m + 7) / 8), std::max(occ, 1) * h->num_sms));
+        Work wk{nullptr, (int32_t)m, h->cursors + 2 * NBINS};
+        const Tail tail = make_tail(h);
+        ++g_launches;
+        kern<<<grid, 256, smem, st>>>(h->prob, o, wk, cap_lg, tail);
+        CU(cudaGetLastError());
+        trace("tiny1");
+        if ((rc = wait_tail(h, st, tail.seq))) return rc;
+        if (!h->h_summary->pad) {
+            h->compacted = h->early_idx != nullptr;
+            h->sum = *h->h_summary;
+            mark(h, 1);
+            mark(h, 2);
+            mark(h, 3);
+            h->stats = mm_stats_t{};
+            h->stats.generated_flops = (int64_t)h->sum.gen_flops;
+            h->stats.rows_empty = h->sum.bin_count[BIN_EMPTY];
+            h->stats.rows_push = m - h->stats.rows_empty;
+            h->total_nnz = h->sum.total_nnz;
+            h->stats.evaluated_multiplies = (int64_t)h->sum.evaluated;
+            h->bound_flag = h->sum.flag;
+            // profile: every non-empty row ran the 1-warp plain hash kernel
+            h->sum.bin_count[hash_bin(MODE_PLAIN, 0, 0)] = (int)h->stats.rows_push;
+            h->sum.bin_flops[hash_bin(MODE_PLAIN, 0, 0)] = h->sum.gen_flops;
+            trace("sync2");
+            mark(h, 4);
+            *out_nnz = h->total_nnz;
+            h->active = true;
+            return MM_OK;
+        }
+        // a mask row over half the fixed table: the whole multiply runs the binned path
+        fused_overflow = true;
+        CU(cudaMemsetAsync(h->d_summary, 0, zero_bytes, st));
+    }
     if ((rc = run_analysis())) return rc;
     // ---- small plain one-phase problems: one pass over every row with a
     // fixed single-warp table, one host sync (no binning round trip).  A row
     // whose mask does not fit sets the overflow flag and the multiply falls
     // back to the binned path below (the analysis summary is already there).
     // (a hash accumulator: only the plans that name one, or leave the choice)
-    const bool tiny = !direct && plain_1p && m > 0 && m <= h->tiny_rows && mask->nnz <= h->tiny_nnz &&
-                      a->nnz <= h->tiny_nnz && (plan->algorithm == MM_ALGO_AUTO || plan->algorithm == MM_ALGO_HASH);
+    const bool tiny = tiny_ok && !fused_overflow;
     if (tiny) {
         h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)
         Out o{};
@@ -1316,6 +1459,20 @@ int mm_create(int device, mm_handle_t** out) {
         delete h;
         return fail(MM_ERR_CUDA, "cudaMallocHost failed");
     }
+    // fused tail: a device ticket counter and the mapped host words its last
+    // block writes; without them (no mapped memory) the separate kernels run
+    if (cudaHostAlloc((void**)&h->h_tail, sizeof(TailResult), cudaHostAllocMapped) == cudaSuccess) {
+        std::memset(h->h_tail, 0, sizeof(TailResult));
+        if (cudaMalloc((void**)&h->d_done, sizeof(unsigned)) != cudaSuccess ||
+            cudaMemset(h->d_done, 0, sizeof(unsigned)) != cudaSuccess) {
+            cudaGetLastError();
+            if (h->d_done) cudaFree(h->d_done);
+            h->d_done = nullptr;
+        }
+    } else {
+        cudaGetLastError();
+        h->h_tail = nullptr;
+    }
     *out = h;
     return MM_OK;
 }
@@ -1325,8 +1482,11 @@ int mm_destroy(mm_handle_t* h) {
     DeviceGuard dg(h->device);
     if (h->active) release(h);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->tail_stream) cudaStreamSynchronize(h->tail_stream);
     cudaFreeHost(h->h_summary);
     cudaFreeHost(h->h_scalar);
+    if (h->h_tail) cudaFreeHost(h->h_tail);
+    if (h->d_done) cudaFree(h->d_done);
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
     if (h->fork_ev) {
         cudaEventDestroy(h->fork_ev);
@@ -1420,6 +1580,8 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 14 && params[14] >= 0) h->direct_on = params[14] != 0;
     if (n > 15 && params[15] >= 0) h->slice_cursors = params[15] != 0;
     if (n > 16 && params[16] >= 0) h->split_slices = params[16] != 0;
+    if (n > 17 && params[17] >= 0) h->fused_rows = params[17];  // 0 disables the one-launch path (fused_tail.cuh)
+    if (n > 18 && params[18] >= 0) h->fused_nnz = params[18];
     return MM_OK;
 }
 

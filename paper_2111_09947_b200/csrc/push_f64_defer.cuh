@@ -30,6 +30,7 @@
 #pragma once
 #include "analyze.cuh"
 #include "common.cuh"
+#include "fused_tail.cuh"
 #include "product_loop.cuh"
 
 namespace mm {
@@ -231,8 +232,12 @@ __device__ __forceinline__ int defer_fold_emit(int n, const DeferWarp& w, const 
 // into o.gen_flops / o.empty_rows, and a row whose mask exceeds nm_max or
 // whose products exceed flops_cap raises o.overflow (the host then runs the
 // binned path instead).
-template <bool NUMERIC>
-__global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work wk, int nm_max, long long flops_cap) {
+//
+// TAIL: the last block also runs the fused tail (fused_tail.cuh: scan,
+// compaction and the counters written to mapped host memory).
+template <bool NUMERIC, bool TAIL = false>
+__global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work wk, int nm_max, long long flops_cap,
+                                                           Tail tail) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -375,6 +380,7 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
         if (gen) atomicAdd(o.gen_flops, gen);
         if (empty) atomicAdd(o.empty_rows, empty);
     }
+    if (TAIL) fused_tail(tail, (int*)smem);
 }
 
 }  // namespace mm

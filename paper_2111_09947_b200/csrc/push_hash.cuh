@@ -22,6 +22,7 @@
 #pragma once
 #include "analyze.cuh"
 #include "common.cuh"
+#include "fused_tail.cuh"
 #include "product_loop.cuh"
 
 namespace mm {
@@ -857,6 +858,77 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
         long long e = warp_sum_ll((long long)evaluated);
         if ((threadIdx.x & 31) == 0 && e) atomicAdd(o.evaluated, (unsigned long long)e);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Small plain one-phase multiplies in ONE launch: the 1-warp plain hash kernel
+// over every row (no analysis pass: the warp sums the row's products itself,
+// as flops_per_row does, multiply.py:103-108) followed by the fused tail
+// (fused_tail.cuh).  A mask row over half the fixed table raises o.overflow
+// and the host runs the binned path instead.
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(256, MM_HASH_MINB)
+k_tiny_hash(Prob p, Out o, Work wk, int cap_lg_max, Tail tail) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int GW = 1, GT = 32;
+    const int groups = blockDim.x / GT;
+    const int g = threadIdx.x / GT;
+    const int gt = threadIdx.x % GT;
+    const int cap_max = 1 << cap_lg_max;
+    constexpr size_t BATCH_BYTES = batch_bytes<GW, KIND>();
+    unsigned char* base = smem + (size_t)g * cap_max * HashEntry<KIND>::bytes;
+    unsigned char* bbase = smem + (size_t)groups * cap_max * HashEntry<KIND>::bytes + (size_t)g * BATCH_BYTES;
+    BatchSmem bsm = bind_batch<GW, KIND>(bbase);
+    unsigned char* wq = smem + (size_t)groups * cap_max * HashEntry<KIND>::bytes + (size_t)groups * BATCH_BYTES +
+                        (size_t)g * queue_bytes<KIND>();
+    Table<KIND> tb;
+    tb.bind(base, cap_max);
+    __shared__ uint32_t s_dummy[256];
+    const uint32_t dummy_s = (uint32_t)__cvta_generic_to_shared(s_dummy + threadIdx.x);
+    if (KIND != 2) {   // hash_row keeps the table clean from here on
+        for (int e = gt; e < cap_max; e += GT) {
+            tb.keys[e] = EMPTY_KEY;
+            tb.cnt[e] = 0;
+            if (KIND == 1) tb.val[e] = 0ull;
+        }
+        __syncwarp();
+    }
+    unsigned long long evaluated = 0, gen = 0;
+    int empty = 0;
+    RowFetcher<GW> rf;
+    if (wk.count < 4 * (int)(gridDim.x * groups)) rf.per = 1;
+    RowInfo ri;
+    while (rf.next(p, wk, gt, 0, nullptr, ri)) {
+        long long f = 0;
+        for (int64_t t = ri.as + gt; t < ri.ae; t += 32) {
+            const int32_t k = p.a_idx[t];
+            f += p.b_ptr[k + 1] - p.b_ptr[k];
+        }
+        f = warp_sum_ll(f);
+        gen += (unsigned long long)f;
+        if (f == 0 || ri.me == ri.ms) {   // no products / empty mask row (_kernels.py:143-145)
+            empty++;
+            if (gt == 0) o.row_nnz[ri.i] = 0;
+            continue;
+        }
+        if (ri.me - ri.ms > (1 << (cap_lg_max - 1))) {
+            if (gt == 0) {
+                atomicExch(o.overflow, 1);
+                o.row_nnz[ri.i] = 0;
+            }
+            continue;
+        }
+        hash_row<GW, KIND, MODE_PLAIN, true, true>(p, o, tb, ri, cap_lg_max, cap_lg_max, gt, 0, nullptr, bsm, wq,
+                                                   dummy_s, evaluated, nullptr);
+    }
+    const long long e = warp_sum_ll((long long)evaluated);
+    if (gt == 0) {
+        if (e) atomicAdd(o.evaluated, (unsigned long long)e);
+        if (gen) atomicAdd(o.gen_flops, gen);
+        if (empty) atomicAdd(o.empty_rows, empty);
+    }
+    fused_tail(tail, (int*)smem);
 }
 
 }  // namespace mm
