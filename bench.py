@@ -11,7 +11,9 @@ binning, numeric kernels, row-pointer scan, nnz readback, exact-size C,
 compaction) plus the device reduction of sum(C).  Inputs are resident in HBM
 when the timed region starts (`value`); `e2e` repeats the step through the
 public API from pinned HOST buffers with the host->device copies and the
-device->host read of the triangle count inside the timed region.
+device->host read of the triangle count inside the timed region (N = 1:
+graphs.triangle_count_lower_streamed — L is strictly lower triangular, so its
+first row block multiplies while the rest of L is still being copied).
 
     python bench.py [--gpus N --steps K --warmup W]       # ours (default)
     python bench.py --impl reference                      # CPU oracle arm
@@ -58,6 +60,10 @@ def parse():
     ap.add_argument("--scale", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-upload", default="streamed", choices=["streamed", "whole"],
+                    help="N = 1 e2e: upload of L pipelined with the row-block multiplies "
+                         "(graphs.triangle_count_lower_streamed) or copied whole before one multiply")
+    ap.add_argument("--e2e-first", type=float, default=0.2, help="share of L's entries in the first uploaded block")
     return ap.parse_args()
 
 
@@ -241,6 +247,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2111_09947_b200.device import DeviceCsr
     from paper_2111_09947_b200.distributed import (RowPartition, allreduce_sum_, broadcast_csr,
                                                    replicate_from_host, row_work_device)
+    from paper_2111_09947_b200.graphs import triangle_count_lower_streamed
     from paper_2111_09947_b200.multiply import _handle, multiply_device, reduce_sum
 
     # one process per GPU; MM_DIST_BACKEND=gloo (with fewer GPUs than ranks)
@@ -386,14 +393,21 @@ def run_ours(args, rank, world, local_rank):
             e0.record(stream)
             if world > 1:
                 replicate_from_host([h_ptr, h_idx] if rank == 0 else None, [e_ptr, e_idx])
-            else:
+            elif args.e2e_upload == "whole":
                 e_ptr.copy_(h_ptr, non_blocking=True)
                 e_idx.copy_(h_idx, non_blocking=True)
-            d_full = DeviceCsr(m, ncols, e_ptr, e_idx, None)
-            d_a = part.block(d_full) if world > 1 else d_full
-            d_bt = d_full.transpose_storage() if args.algo == "inner" else None
-            _, _, tri_e = step(d_a, d_full, d_bt)
-            tri_host = int(tri_e.item())                   # device->host read of the result
+            if world == 1 and args.e2e_upload == "streamed":
+                # L is strictly lower triangular: rows [0, r) need only rows [0, r) of
+                # B = L, so the first block multiplies while the rest is on the wire
+                tri_host = triangle_count_lower_streamed(h_ptr, h_idx, plan, device=dev,
+                                                         first_fraction=args.e2e_first,
+                                                         buffers=(e_ptr, e_idx)).value
+            else:
+                d_full = DeviceCsr(m, ncols, e_ptr, e_idx, None)
+                d_a = part.block(d_full) if world > 1 else d_full
+                d_bt = d_full.transpose_storage() if args.algo == "inner" else None
+                _, _, tri_e = step(d_a, d_full, d_bt)
+                tri_host = int(tri_e.item())               # device->host read of the result
             e1.record(stream)
             e1.synchronize()
             if s > 0:
@@ -406,10 +420,15 @@ def run_ours(args, rank, world, local_rank):
             e2e_t = float(t.item())
         h2d = (m + 1) * 8 + nnz_l * 4                       # rank 0's copy of L
         e2e = {"value": evaluated / (e2e_t * 1e-3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": world * (8 + 2 * SUMMARY_BYTES),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": (8 + 4 * SUMMARY_BYTES if world == 1 and args.e2e_upload == "streamed"
+                                      else world * (8 + 2 * SUMMARY_BYTES)),
                "ms_per_step": e2e_t,
                "path": ("H2D of L on rank 0 + NCCL broadcast + per-rank block multiply + all-reduce"
-                        if world > 1 else "H2D of L + multiply + device sum + D2H of the count")}
+                        if world > 1 else
+                        ("H2D of L in two pieces, the first row block (%.0f %% of the entries) multiplied while the "
+                         "second piece is copied, second block, device sums + D2H of the count" % (100 * args.e2e_first)
+                         if args.e2e_upload == "streamed"
+                         else "H2D of L + multiply + device sum + D2H of the count"))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -106,3 +106,30 @@ def test_ewise_add_shape_mismatch():
     b = DeviceCsr.from_host(random_csr(rng, 5, 4, 2).astype(np.float64), dtype=np.float64)
     with pytest.raises(SparseError):
         ewise_add(a, b)
+
+
+@pytest.mark.parametrize("first", [0.0, 0.2, 0.5, 1.0])
+@pytest.mark.parametrize("algo", ["auto", "hash", "inner"])
+def test_triangle_count_streamed_upload(first, algo):
+    """graphs.triangle_count_lower_streamed: the upload of L pipelined with the
+    row-block multiplies gives the count of the single multiply (reference
+    graphs.py:87-96; rows are independent, multiply.py:8-11, and L is strictly
+    lower triangular, so a row block needs only the rows of B above its end)."""
+    import oracle
+    from paper_2111_09947_b200 import MultiplyPlan, plus_pair_semiring
+    from paper_2111_09947_b200.graphs import triangle_count_lower_streamed
+    from paper_2111_09947_b200.sparse import degree_sort_relabel, simple_undirected_graph, tril_strict
+    from paper_2111_09947_b200.workloads import GeneratorSpec, generate
+    plan = MultiplyPlan(algorithm=algo, semiring=plus_pair_semiring(np.int64))
+    for spec, want in ((GeneratorSpec("erdos-renyi", 10, 8, seed=42), 618), (GeneratorSpec("rmat", 13, 16, seed=3), None)):
+        g = simple_undirected_graph(generate(spec))
+        low = tril_strict(degree_sort_relabel(g)[0])
+        if want is None:
+            r = oracle.masked_multiply(low.pattern(), low, low, semiring_id=1)
+            want = int(r.values.sum())
+        h_ptr = torch.from_numpy(np.ascontiguousarray(low.row_ptr, dtype=np.int64)).pin_memory()
+        h_idx = torch.from_numpy(np.ascontiguousarray(low.col_idx[: low.nnz], dtype=np.int32)).pin_memory()
+        for rep in range(3):
+            res = triangle_count_lower_streamed(h_ptr, h_idx, plan, first_fraction=first)
+            assert res.value == want
+            assert res.multiplies in (1, 2) and (res.multiplies == 1 or (first > 0.0 and algo != "inner"))
