@@ -1075,8 +1075,13 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     const double est_push = (double)a->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->nrows, 1));
     const double est_pull = (double)mask->nnz * ((double)b->nnz / (double)std::max<int64_t>(b->ncols, 1) +
                                                  (double)a->nnz / (double)std::max<int64_t>(m, 1));
+    // ... and only when the mask is neither nearly empty (under a quarter of
+    // the rows can have an entry: the analysis never launches the others,
+    // the direct kernel would walk their A rows to count products) nor mostly
+    // wider than the kernel's 128-entry rows (batched BC's backward steps)
+    const bool mask_fits = 4 * mask->nnz >= m && mask->nnz <= 64 * m;
     const bool direct = plain_1p && h->kind == 2 && m > 0 && h->direct_on && (!use_bt || 3.0 * est_pull >= est_push) &&
-                        plan->algorithm == MM_ALGO_AUTO;
+                        plan->algorithm == MM_ALGO_AUTO && mask_fits;
     bool have_summary = false;
     if (direct) {
         h->bound_off = mask->ptr;   // bounds = mask row lengths (multiply.py:233)

@@ -235,6 +235,8 @@ __device__ __forceinline__ int defer_fold_emit(int n, const DeferWarp& w, const 
 //
 // TAIL: the last block also runs the fused tail (fused_tail.cuh: scan,
 // compaction and the counters written to mapped host memory).
+constexpr int64_t DIRECT_MAX_NA = 1024;
+
 template <bool NUMERIC, bool TAIL = false>
 __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work wk, int nm_max, long long flops_cap,
                                                            Tail tail) {
@@ -257,7 +259,11 @@ __global__ void __launch_bounds__(256, 4) k_push_f64_defer(Prob p, Out o, Work w
     while (rf.next(p, wk, lane, 0, nullptr, ri)) {
         const int64_t ms = ri.ms;
         const int nm = (int)(ri.me - ms);
-        if (flops_cap && nm > nm_max) {
+        // direct mode: wide mask rows, and rows with so many A entries that one
+        // warp would walk them for milliseconds just to count their products
+        // (R-MAT hubs under a nearly empty mask: a batched-BC backward step),
+        // go to the binned pass, whose analysis takes a block per long row
+        if (flops_cap && (nm > nm_max || ri.ae - ri.as > DIRECT_MAX_NA)) {
             if (lane == 0) {
                 atomicExch(o.overflow, 1);
                 o.row_nnz[ri.i] = -1;   // left to the binned pass

@@ -581,3 +581,34 @@ def test_plan_runs_its_accumulator():
                     allowed = prefixes + (("hash_ctab", "hash_csrch") if comp and algo == "msa" else ())
                     bad = [k for k in used if not k.startswith(allowed)]
                     assert not bad, (algo, comp, sem.name, str(sem.dtype), used)
+
+
+def test_direct_float64_long_a_rows_go_to_the_binned_pass():
+    """Direct float64 path (no analysis pass): rows with more than 1024 A
+    entries (one warp would walk them alone) and rows with wide masks are left
+    to the binned pass; everything still equals the oracle bit for bit, counters
+    included (reference order: _kernels.py:48-65)."""
+    from paper_2111_09947_b200.multiply import last_kernel_rows
+    rng = np.random.default_rng(77)
+    m, n = 3000, 3000
+    lens = rng.integers(1, 12, m)
+    lens[[5, 1700]] = [2500, 1100]          # two hub rows of A
+    a_r = np.repeat(np.arange(m), lens)
+    a_c = np.concatenate([rng.choice(n, ln, replace=False) for ln in lens])
+    a = from_arrays(m, n, a_r, a_c, rng.standard_normal(a_c.size))
+    b_r = np.repeat(np.arange(n), rng.integers(1, 10, n))
+    b = from_arrays(n, n, b_r, rng.integers(0, n, b_r.size), rng.standard_normal(b_r.size))
+    m_len = rng.integers(0, 4, m)
+    m_len[[5, 9]] = [40, 300]               # a hub row with a mask, a wide mask row
+    m_r = np.repeat(np.arange(m), m_len)
+    m_c = np.concatenate([rng.choice(n, ln, replace=False) for ln in m_len])
+    mask = from_arrays(m, n, m_r, m_c, np.ones(m_c.size, dtype=np.int64)).pattern()
+    sem = arithmetic_semiring(np.float64)
+    c, st = masked_multiply_with_stats(mask, a, b, MultiplyPlan(algorithm="auto", semiring=sem))
+    rows = last_kernel_rows()
+    r = oracle.masked_multiply(mask, a, b, algorithm="msa", dtype=np.float64)
+    assert np.array_equal(c.row_ptr, r.row_ptr)
+    assert np.array_equal(c.col_idx[: c.nnz], r.col_idx)
+    assert np.array_equal(c.values[: c.nnz], r.values)
+    assert (st.generated_flops, st.evaluated_multiplies) == (r.generated_flops, r.evaluated_multiplies)
+    assert sum(v for k, v in rows.items() if k != "empty") >= 1, rows
