@@ -133,7 +133,13 @@ int mm_multiply_end(mm_handle_t* h, int64_t* c_row_ptr, int32_t* c_col_idx, void
  * nrows + 1 (written by the row-pointer scan itself); one host sync (the
  * nnz readback), compaction queued right after it.  If nnz(C) > capacity it
  * returns MM_ERR_CAPACITY with *out_nnz set and the handle still holding
- * the multiply: allocate nnz(C) entries and finish with mm_multiply_end. */
+ * the multiply: allocate nnz(C) entries and finish with mm_multiply_end.
+ * Like every entry point the results are ordered on `stream`: the smallest
+ * plain one-phase multiplies run as ONE launch whose last block reports the
+ * counters through mapped host memory, and the call may return as soon as
+ * they arrive, before that launch has retired — use C on `stream`, or
+ * synchronise it first (the handle itself waits when the next multiply names
+ * another stream). */
 int mm_multiply(mm_handle_t* h, const mm_plan_t* plan, const mm_matrix_t* mask, const mm_matrix_t* a,
                 const mm_matrix_t* b, const mm_matrix_t* b_csc, void* stream, int64_t* c_row_ptr,
                 int32_t* c_col_idx, void* c_values, int64_t capacity, int64_t* out_nnz, mm_stats_t* stats);
