@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--e2e-upload", default="streamed", choices=["streamed", "whole"],
                     help="N = 1 e2e: upload of L pipelined with the row-block multiplies "
                          "(graphs.triangle_count_lower_streamed) or copied whole before one multiply")
-    ap.add_argument("--e2e-first", type=float, default=0.2, help="share of L's entries in the first uploaded block")
+    ap.add_argument("--e2e-first", default="0.2",
+                    help="share of L's entries in the first uploaded block; a comma list of increasing shares cuts more blocks")
     return ap.parse_args()
 
 
@@ -379,6 +380,7 @@ def run_ours(args, rank, world, local_rank):
     # rank multiplies its row block (views, host-known offsets) -> device sum
     # -> NCCL all-reduce -> D2H of the count.
     e2e = None
+    e2e_shares = [float(x) for x in str(args.e2e_first).split(",")]
     if not args.no_e2e:
         e_ptr = torch.empty(m + 1, dtype=torch.int64, device=dev)
         e_idx = torch.empty(nnz_l, dtype=torch.int32, device=dev)
@@ -400,7 +402,7 @@ def run_ours(args, rank, world, local_rank):
                 # L is strictly lower triangular: rows [0, r) need only rows [0, r) of
                 # B = L, so the first block multiplies while the rest is on the wire
                 tri_host = triangle_count_lower_streamed(h_ptr, h_idx, plan, device=dev,
-                                                         first_fraction=args.e2e_first,
+                                                         first_fraction=e2e_shares,
                                                          buffers=(e_ptr, e_idx)).value
             else:
                 d_full = DeviceCsr(m, ncols, e_ptr, e_idx, None)
@@ -420,13 +422,14 @@ def run_ours(args, rank, world, local_rank):
             e2e_t = float(t.item())
         h2d = (m + 1) * 8 + nnz_l * 4                       # rank 0's copy of L
         e2e = {"value": evaluated / (e2e_t * 1e-3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": (8 + 4 * SUMMARY_BYTES if world == 1 and args.e2e_upload == "streamed"
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": (8 + 2 * (len(e2e_shares) + 1) * SUMMARY_BYTES
+                                      if world == 1 and args.e2e_upload == "streamed"
                                       else world * (8 + 2 * SUMMARY_BYTES)),
                "ms_per_step": e2e_t,
                "path": ("H2D of L on rank 0 + NCCL broadcast + per-rank block multiply + all-reduce"
                         if world > 1 else
-                        ("H2D of L in two pieces, the first row block (%.0f %% of the entries) multiplied while the "
-                         "second piece is copied, second block, device sums + D2H of the count" % (100 * args.e2e_first)
+                        ("H2D of L in %d pieces (cut at %s of the entries), each row block multiplied while the "
+                         "next piece is copied, device sums + D2H of the count" % (len(e2e_shares) + 1, args.e2e_first)
                          if args.e2e_upload == "streamed"
                          else "H2D of L + multiply + device sum + D2H of the count"))}
 

@@ -87,7 +87,7 @@ def triangle_count(g: CsrMatrix, plan: MultiplyPlan, device=None) -> KernelResul
 _copy_streams: dict = {}
 
 
-def triangle_count_lower_streamed(h_ptr, h_idx, plan: MultiplyPlan, device=None, first_fraction: float = 0.2,
+def triangle_count_lower_streamed(h_ptr, h_idx, plan: MultiplyPlan, device=None, first_fraction=0.2,
                                   buffers=None) -> KernelResult:
     """sum(L (.) (L L)) for a HOST-resident strict lower triangle L, the upload
     pipelined with the multiply (graphs.py:87-96 from the multiply on).
@@ -99,6 +99,8 @@ def triangle_count_lower_streamed(h_ptr, h_idx, plan: MultiplyPlan, device=None,
     its row block is multiplied while the rest of L is still on the wire, then
     the second block runs.  Same products, same C rows, same count as one
     multiply (tests/test_gpu_graph_ops.py); only the upload overlaps.
+    ``first_fraction`` may be a sequence of increasing shares (cut points):
+    (0.05, 0.25) uploads and multiplies three row blocks.
     ``buffers`` = (ptr, idx) device tensors to upload into (else allocated).
     (Running the second block from a helper thread on a second stream, so the
     two multiplies overlap, measured 1.5 % faster on average but erratic —
@@ -118,31 +120,39 @@ def triangle_count_lower_streamed(h_ptr, h_idx, plan: MultiplyPlan, device=None,
         d_idx = torch.empty(nnz, dtype=torch.int32, device=dev)
     else:
         d_ptr, d_idx = buffers
-    # split row: the first row whose offset reaches the requested share of the entries
-    r = int(np.searchsorted(ptr_np, int(first_fraction * nnz), side="left"))
-    r = min(max(r, 0), m)
+    # cut rows: the first row whose offset reaches each requested share of the entries
+    shares = [first_fraction] if np.isscalar(first_fraction) else list(first_fraction)
     if kplan.algorithm == "inner":
-        r = 0   # the pull path transposes all of B first: nothing to overlap
-    p1 = int(ptr_np[r])
+        shares = []   # the pull path transposes all of B first: nothing to overlap
+    cuts = [0]
+    for f in shares:
+        r = int(np.searchsorted(ptr_np, int(min(max(float(f), 0.0), 1.0) * nnz), side="left"))
+        cuts.append(min(max(r, cuts[-1]), m))
+    cuts.append(m)
+    offs = [int(ptr_np[r]) for r in cuts]
     cur = torch.cuda.current_stream(dev)
     cs = _copy_streams.get(dev.index)
     if cs is None:
         cs = _copy_streams[dev.index] = torch.cuda.Stream(dev)
     cs.wait_stream(cur)
-    e1, e2 = torch.cuda.Event(), torch.cuda.Event()
+    events = []
     with torch.cuda.stream(cs):
-        # the first block reads row offsets 0..r only (its own rows and the B rows above r)
-        d_ptr[: r + 1].copy_(h_ptr[: r + 1], non_blocking=True)
-        d_idx[:p1].copy_(h_idx[:p1], non_blocking=True)
-        e1.record(cs)
-        d_ptr[r + 1:].copy_(h_ptr[r + 1:], non_blocking=True)
-        d_idx[p1:].copy_(h_idx[p1:], non_blocking=True)
-        e2.record(cs)
+        for q in range(len(cuts) - 1):
+            lo, hi, q0, q1 = cuts[q], cuts[q + 1], offs[q], offs[q + 1]
+            # a block reads row offsets up to its last row only (its own rows and the B rows above them)
+            p_lo = lo + 1 if q else 0
+            if hi + 1 > p_lo:
+                d_ptr[p_lo: hi + 1].copy_(h_ptr[p_lo: hi + 1], non_blocking=True)
+            if q1 > q0:
+                d_idx[q0:q1].copy_(h_idx[q0:q1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append(ev)
     full = DeviceCsr(m, m, d_ptr, d_idx, None)
     res = KernelResult(0)
-
     total = None
-    for lo, hi, q0, q1, ev in ((0, r, 0, p1, e1), (r, m, p1, nnz, e2)):
+    for q, ev in enumerate(events):
+        lo, hi, q0, q1 = cuts[q], cuts[q + 1], offs[q], offs[q + 1]
         cur.wait_event(ev)
         if hi == lo:
             continue
