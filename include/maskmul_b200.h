@@ -172,7 +172,9 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
  * group instead of as (row, slice) work items,
  * params[17] / params[18] = row / nnz limits of the one-launch path for the
  * smallest plain one-phase multiplies (8192 / 2^17; 0 disables it): the row
- * kernel's last block scans, compacts and reports through mapped host memory. */
+ * kernel's last block scans, compacts and reports through mapped host memory,
+ * params[19] = 0 makes the analysis gather B's 8-byte row offsets instead of
+ * the int32 row lengths it otherwise derives first. */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

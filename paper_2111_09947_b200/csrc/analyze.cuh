@@ -93,7 +93,20 @@ struct AnalyzeParams {
     int vbytes;      // value bytes read per operand entry (0 plus-pair, 8 otherwise)
     int has_bt;      // B^T (CSC) available
     const int64_t* done;   // rows with done[i] >= 0 were computed already (direct pass): skipped
+    const int32_t* b_len;  // nnz(B_k*) per row of B (k_row_len), or null: the analysis gathers one
+                           // 4-byte length per A entry instead of two 8-byte offsets (half the sectors)
 };
+
+// Row lengths of B as int32 (nnz(B) < 2^31 is validated).
+__global__ void __launch_bounds__(256) k_row_len(int64_t nrows, const int64_t* ptr, int32_t* len) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x)
+        len[i] = (int32_t)(ptr[i + 1] - ptr[i]);
+}
+
+template <bool BLEN>
+__device__ __forceinline__ long long b_row_len(const Prob& p, const AnalyzeParams& ap, int32_t k) {
+    return BLEN ? (long long)__ldg(ap.b_len + k) : (long long)(p.b_ptr[k + 1] - p.b_ptr[k]);
+}
 
 __host__ __device__ __forceinline__ int tier_cap_lg(int pair, int tier) {
     return pair ? tier_cap_lg_pair(tier) : tier_cap_lg_val(tier);
@@ -267,6 +280,7 @@ constexpr int64_t LONG_ROW = 2048;
 
 // One warp per row.  Computes row_flops, 1P complement bounds, bin + table size.
 // Long rows are appended to long_rows[] (count in long_rows_n) instead.
+template <bool BLEN>
 __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64_t* row_flops,
                                                  int64_t* bound, uint8_t* row_bin, int8_t* row_cap_lg,
                                                  Summary* s, int64_t* row_nnz, int32_t* long_rows,
@@ -313,12 +327,11 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
             int64_t t = as;
             for (; t + 4 <= ae; t += 4) {
                 const int32_t k0 = p.a_idx[t], k1 = p.a_idx[t + 1], k2 = p.a_idx[t + 2], k3 = p.a_idx[t + 3];
-                f += (p.b_ptr[k0 + 1] - p.b_ptr[k0]) + (p.b_ptr[k1 + 1] - p.b_ptr[k1]) +
-                     (p.b_ptr[k2 + 1] - p.b_ptr[k2]) + (p.b_ptr[k3 + 1] - p.b_ptr[k3]);
+                f += b_row_len<BLEN>(p, ap, k0) + b_row_len<BLEN>(p, ap, k1) + b_row_len<BLEN>(p, ap, k2) + b_row_len<BLEN>(p, ap, k3);
             }
             for (; t < ae; t++) {
                 const int32_t k = p.a_idx[t];
-                f += p.b_ptr[k + 1] - p.b_ptr[k];
+                f += b_row_len<BLEN>(p, ap, k);
             }
         }
         unsigned longm = __ballot_sync(FULL, ae - as > 32);
@@ -329,7 +342,7 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
             long long g = 0;
             for (int64_t t = s0 + lane; t < s1; t += 32) {
                 const int32_t k = p.a_idx[t];
-                g += p.b_ptr[k + 1] - p.b_ptr[k];
+                g += b_row_len<BLEN>(p, ap, k);
             }
             g = warp_sum_ll(g);
             if (lane == src) f = g;
@@ -431,6 +444,7 @@ __global__ void __launch_bounds__(256) k_analyze(Prob p, AnalyzeParams ap, int64
 // Long rows (see LONG_ROW): one block per row, same quantities and the same
 // classification as k_analyze, folded into the summary with global atomics.
 // Runs after k_analyze on the same stream; grid-strides over the list.
+template <bool BLEN>
 __global__ void __launch_bounds__(256) k_analyze_long(Prob p, AnalyzeParams ap, int64_t* row_flops,
                                                       int64_t* bound, uint8_t* row_bin, int8_t* row_cap_lg,
                                                       Summary* s, int64_t* row_nnz, const int32_t* long_rows,
@@ -446,12 +460,11 @@ __global__ void __launch_bounds__(256) k_analyze_long(Prob p, AnalyzeParams ap, 
         int64_t t = as + threadIdx.x;
         for (; t + 3 * 256 < ae; t += 4 * 256) {
             const int32_t k0 = p.a_idx[t], k1 = p.a_idx[t + 256], k2 = p.a_idx[t + 512], k3 = p.a_idx[t + 768];
-            f += (p.b_ptr[k0 + 1] - p.b_ptr[k0]) + (p.b_ptr[k1 + 1] - p.b_ptr[k1]) +
-                 (p.b_ptr[k2 + 1] - p.b_ptr[k2]) + (p.b_ptr[k3 + 1] - p.b_ptr[k3]);
+            f += b_row_len<BLEN>(p, ap, k0) + b_row_len<BLEN>(p, ap, k1) + b_row_len<BLEN>(p, ap, k2) + b_row_len<BLEN>(p, ap, k3);
         }
         for (; t < ae; t += 256) {
             const int32_t k = p.a_idx[t];
-            f += p.b_ptr[k + 1] - p.b_ptr[k];
+            f += b_row_len<BLEN>(p, ap, k);
         }
         f = warp_sum_ll(f);
         if (lane == 0) s_red[wid] = f;

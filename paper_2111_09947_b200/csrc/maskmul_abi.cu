@@ -201,6 +201,7 @@ struct mm_handle {
     int32_t* early_idx = nullptr;                       // mm_multiply, small plain 1P: C's arrays, compacted
     void* early_val = nullptr;                          //   before the single host sync
     bool compacted = false;
+    bool blen_on = true;                                // analysis gathers int32 row lengths of B (k_row_len)
     int64_t mask_nnz = 0;
     // ---- fused tail (fused_tail.cuh): one-launch small plain 1P multiplies ----
     unsigned* d_done = nullptr;          // device ticket counter, zero between multiplies
@@ -1002,6 +1003,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     ap.vbytes = pair ? 0 : 8;
     ap.has_bt = use_bt;
     ap.done = nullptr;
+    ap.b_len = nullptr;
     const int64_t m = h->nrows;
 
     // One pool allocation carves every per-multiply array; summary and fetch
@@ -1024,6 +1026,10 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     const size_t o_rows = carve(m * sizeof(int32_t));
     const size_t o_bin = carve(m);
     const size_t o_cap = carve(m);
+    // int32 row lengths of B for the analysis (one 4-byte gather per A entry
+    // instead of two 8-byte offsets): pays when A has several entries per row of B
+    const bool use_blen = h->blen_on && a->nnz >= 4 * b->nrows && a->nnz >= (1 << 20);
+    const size_t o_blen = use_blen ? carve((size_t)b->nrows * sizeof(int32_t)) : 0;
     const size_t o_tidx = plain_1p ? carve(mask->nnz * sizeof(int32_t)) : 0;
     const size_t o_tval = plain_1p ? carve(mask->nnz * 8) : 0;
     unsigned char* slab = nullptr;
@@ -1050,17 +1056,34 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
 
     auto run_analysis = [&]() -> int {
         if (m <= 0) return MM_OK;
+        if (use_blen && !ap.b_len) {
+            int32_t* blen = (int32_t*)(slab + o_blen);
+            const int bg = (int)std::max<int64_t>(1, std::min<int64_t>((b->nrows + 255) / 256, (int64_t)h->num_sms * 8));
+            ++g_launches;
+            k_row_len<<<bg, 256, 0, st>>>(b->nrows, b->ptr, blen);
+            CU(cudaGetLastError());
+            ap.b_len = blen;
+        }
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)h->num_sms * 8));
         int64_t* zero_nnz = symbolic_only ? nullptr : h->row_nnz;
         ++g_launches;
-        k_analyze<<<grid, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin, h->row_cap_lg,
-                                        h->d_summary, zero_nnz, long_rows, long_n);
+        if (ap.b_len)
+            k_analyze<true><<<grid, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin, h->row_cap_lg,
+                                                  h->d_summary, zero_nnz, long_rows, long_n);
+        else
+            k_analyze<false><<<grid, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin, h->row_cap_lg,
+                                                   h->d_summary, zero_nnz, long_rows, long_n);
         CU(cudaGetLastError());
         if (a->nnz > LONG_ROW || (ap.has_bt && mask->nnz > LONG_ROW)) {   // a long row is possible
             ++g_launches;
-            k_analyze_long<<<h->num_sms * 2, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin,
-                                                            h->row_cap_lg, h->d_summary, zero_nnz, long_rows,
-                                                            long_n);
+            if (ap.b_len)
+                k_analyze_long<true><<<h->num_sms * 2, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin,
+                                                                      h->row_cap_lg, h->d_summary, zero_nnz,
+                                                                      long_rows, long_n);
+            else
+                k_analyze_long<false><<<h->num_sms * 2, 256, 0, st>>>(p, ap, h->row_flops, h->bound, h->row_bin,
+                                                                       h->row_cap_lg, h->d_summary, zero_nnz,
+                                                                       long_rows, long_n);
             CU(cudaGetLastError());
         }
         return MM_OK;
@@ -1587,6 +1610,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 16 && params[16] >= 0) h->split_slices = params[16] != 0;
     if (n > 17 && params[17] >= 0) h->fused_rows = params[17];  // 0 disables the one-launch path (fused_tail.cuh)
     if (n > 18 && params[18] >= 0) h->fused_nnz = params[18];
+    if (n > 19 && params[19] >= 0) h->blen_on = params[19] != 0;
     return MM_OK;
 }
 
@@ -1643,9 +1667,9 @@ int mm_row_flops(const mm_matrix_t* a, const mm_matrix_t* b, int64_t* row_flops,
     if (a->nrows > 0) {
         int grid = (int)std::min<int64_t>((a->nrows + 255) / 256, 148 * 8);
         ++g_launches;
-        k_analyze<<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr, long_rows, long_n);
+        k_analyze<false><<<grid, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr, long_rows, long_n);
         ++g_launches;
-        k_analyze_long<<<296, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr, long_rows, long_n);
+        k_analyze_long<false><<<296, 256, 0, st>>>(p, ap, row_flops, nullptr, rb, rc_lg, s, nullptr, long_rows, long_n);
     }
     if (total) CU(cudaMemcpyAsync(total, &s->gen_flops, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     cudaFreeAsync(s, st);
