@@ -124,16 +124,21 @@ __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* b
     const int64_t warp = gtid >> 5;
     const int64_t nwarps = nthreads >> 5;
     constexpr int PER = 128;
-    for (int64_t e0 = warp * PER; e0 < total; e0 += nwarps * PER) {
+    // A warp owns 128-entry tiles: a 32-ary search of the row pointer finds the
+    // row of the tile's first entry; the tile's rows are then read as ONE
+    // coalesced load of the next 32 row ends, and only a tile that spans more
+    // rows (runs of empty rows) searches for its last row.
+    const int64_t tiles = (total + PER - 1) / PER;
+    for (int64_t t = warp; t < tiles; t += nwarps) {
+        // every row before r_lo ends at or before the tile's first entry
+        int64_t r_lo = warp_upper_row(out_ptr, 0, nrows, t * PER, lane);
+        const int64_t e0 = t * PER;
         const int64_t e1 = e0 + PER < total ? e0 + PER : total;
-        // rows holding the tile's first and last entry (last r with out_ptr[r] <= e)
-        const int64_t r_lo = warp_upper_row(out_ptr, 0, nrows, e0, lane);
-        const int64_t r_hi = warp_upper_row(out_ptr, r_lo, nrows, e1 - 1, lane);
-        if (r_hi - r_lo < 32) {
-            // row ends of the span held one per lane; owner by a shuffle search
-            const int64_t r = r_lo + lane;
-            const int64_t end = r <= r_hi ? __ldg(out_ptr + r + 1) : INT64_MAX;
-            const int64_t boff = r <= r_hi ? __ldg(bounds_off + r) - __ldg(out_ptr + r) : 0;
+        const int64_t r = r_lo + lane;
+        const int64_t end = r < nrows ? __ldg(out_ptr + r + 1) : INT64_MAX;
+        if (shfl64(end, 31) > e1 - 1) {
+            // the tile lies within rows r_lo .. r_lo + 31: owner by a shuffle search
+            const int64_t boff = r < nrows ? __ldg(bounds_off + r) - __ldg(out_ptr + r) : 0;
 #pragma unroll
             for (int u = 0; u < PER / 32; u++) {
                 const int64_t e = e0 + u * 32 + lane;
@@ -150,6 +155,8 @@ __global__ void __launch_bounds__(256) k_compact(int64_t nrows, const int64_t* b
                 }
             }
         } else {
+            // a run of more than 32 rows (empty rows among them): search per entry
+            const int64_t r_hi = warp_upper_row(out_ptr, r_lo, nrows, e1 - 1, lane);
 #pragma unroll 4
             for (int u = 0; u < PER / 32; u++) {
                 const int64_t e = e0 + u * 32 + lane;
