@@ -575,7 +575,10 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
             int gw = 1;
             // plain tier-3 rows (int64 / plus-pair): sliced over the 16-warp
             // tier's largest shared table (hash_row), their own launch
-            const bool sliced = tier == 3 && mode == MODE_PLAIN && kind != 2;
+            // (decided by the multiply's kind, not the pass's: the symbolic pass of an
+            // ordered float64 multiply runs as kind 0, but its rows were binned — and
+            // their tables sized — for the global tier)
+            const bool sliced = tier == 3 && mode == MODE_PLAIN && h->kind != 2;
             HashKernel kern = pick_hash(kind, mode, sliced ? 2 : tier, numeric, &gw);
             bool smem_table = tier < 3 || sliced;
             int threads = gw == 32 ? 1024 : (gw == 16 ? 512 : 256);

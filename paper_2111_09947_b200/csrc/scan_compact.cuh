@@ -30,7 +30,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile(const int64_t* in, i
 #pragma unroll
     for (int q = 0; q < SCAN_ITEMS; q++) {
         int64_t idx = base + q;
-        const long long x = idx < n ? in[idx] : 0;
+        // counts are never negative, except the -1 with which the direct float64
+        // pass marks the rows it leaves to the binned pass: those scan as 0, so the
+        // offsets stay monotone and inside C for the compaction queued behind the
+        // scan (its stale rows are rewritten after the binned pass)
+        long long x = idx < n ? in[idx] : 0;
+        x = x > 0 ? x : 0;
         if (bounds_off && idx < n) over |= x > bounds_off[idx + 1] - bounds_off[idx];
         run += x;
         v[q] = run;

@@ -80,3 +80,65 @@ def test_operands_on_second_device_while_first_is_current():
             want = s if want is None else want
             assert s == want
             assert torch.cuda.current_device() == 0
+
+
+def _rand_rows(rng, rows, cols, lens, dtype):
+    import numpy as np
+    from paper_2111_09947_b200 import from_arrays
+    lens = np.minimum(np.asarray(lens), cols)
+    r = np.repeat(np.arange(rows), lens)
+    c = np.concatenate([rng.choice(cols, ln, replace=False) for ln in lens]) if lens.sum() else np.empty(0, np.int64)
+    v = rng.standard_normal(r.size) if dtype == np.float64 else rng.integers(1, 5, r.size)
+    return from_arrays(rows, cols, r, c, v)
+
+
+def test_symbolic_pass_of_float64_multiply_with_global_tier_rows():
+    """Found by tools/fuzz_gpu.py: a float64 plain multiply whose mask rows need the
+    global hash tier (29,654 entries) ran its two-phase symbolic pass (kind 0) as
+    sliced rows over tables sized for the global tier and failed; the tier is
+    decided by the multiply's kind.  Reference: two-phase driver, multiply.py:358-380."""
+    import numpy as np
+    import oracle
+    from paper_2111_09947_b200 import MultiplyPlan, arithmetic_semiring, masked_multiply_with_stats
+    rng = np.random.default_rng(5)
+    m, k, n = 1000, 50, 300000
+    a = _rand_rows(rng, m, k, rng.integers(0, 4, m), np.float64)
+    b = _rand_rows(rng, k, n, rng.integers(10, 50, k), np.float64)
+    mlen = rng.integers(0, 40, m)
+    mlen[[3, 500]] = [29654, 12000]
+    mask = _rand_rows(rng, m, n, mlen, np.int64).pattern()
+    ref = oracle.masked_multiply(mask, a, b, algorithm="msa", dtype=np.float64)
+    for algo in ("auto", "hash", "msa"):
+        for phases in ("1p", "2p"):
+            c, st = masked_multiply_with_stats(mask, a, b, MultiplyPlan(algorithm=algo, phases=phases,
+                                                                      semiring=arithmetic_semiring(np.float64)))
+            assert np.array_equal(c.row_ptr, ref.row_ptr), (algo, phases)
+            assert np.array_equal(c.col_idx[: c.nnz], ref.col_idx), (algo, phases)
+            assert np.array_equal(c.values[: c.nnz], ref.values), (algo, phases)
+            assert st.evaluated_multiplies == ref.evaluated_multiplies
+
+
+def test_direct_pass_leaves_leading_rows_to_the_binned_pass():
+    """Found by tools/fuzz_gpu.py: the direct float64 pass marks rows it cannot take
+    with a count of -1; the scan queued behind it summed those, so the first rows'
+    offsets went negative and the early compaction wrote before C.  Counts below
+    zero scan as zero (scan_compact.cuh).  The leading rows here all have masks over
+    the direct kernel's 128 entries."""
+    import numpy as np
+    import oracle
+    from paper_2111_09947_b200 import MultiplyPlan, arithmetic_semiring, masked_multiply_with_stats
+    rng = np.random.default_rng(6)
+    m, k, n = 20000, 1, 40000
+    a = _rand_rows(rng, m, k, (rng.random(m) < 0.9).astype(np.int64), np.float64)
+    b = _rand_rows(rng, k, n, [9], np.float64)
+    mlen = rng.integers(20, 80, m)
+    mlen[:300] = rng.integers(150, 300, 300)
+    mask = _rand_rows(rng, m, n, mlen, np.int64).pattern()
+    ref = oracle.masked_multiply(mask, a, b, algorithm="msa", dtype=np.float64)
+    for rep in range(3):
+        c, st = masked_multiply_with_stats(mask, a, b, MultiplyPlan(algorithm="auto",
+                                                                  semiring=arithmetic_semiring(np.float64)))
+        assert np.array_equal(c.row_ptr, ref.row_ptr)
+        assert np.array_equal(c.col_idx[: c.nnz], ref.col_idx)
+        assert np.array_equal(c.values[: c.nnz], ref.values)
+        assert (st.generated_flops, st.evaluated_multiplies) == (ref.generated_flops, ref.evaluated_multiplies)
