@@ -82,6 +82,31 @@ while time.time() < t_end:
                                        ev=(st.evaluated_multiplies, ref.evaluated_multiplies),
                                        gen=(st.generated_flops, ref.generated_flops)), flush=True)
                 sys.exit(1)
+    if not comp and not replay_skip and rng.random() < 0.3:
+        # auto with B^T present: the per-row push / pull model on the device
+        from paper_2111_09947_b200.device import DeviceCsr
+        from paper_2111_09947_b200.multiply import multiply_device
+        vals = sem.kernel_id == 0
+        dm = DeviceCsr.from_host(mk, with_values=False)
+        da = DeviceCsr.from_host(a, dtype=dt, with_values=vals)
+        db = DeviceCsr.from_host(b, dtype=dt, with_values=vals)
+        for phases in ("1p", "2p"):
+            plan = MultiplyPlan(algorithm="auto", phases=phases, semiring=sem)
+            try:
+                cd, st = multiply_device(dm, da, db, plan, b_csc=db.transpose_storage())
+                c = cd.to_host()
+            except Exception as e:
+                print("EXCEPTION(bt)", repr(e)[:200], dict(m=m, k=k, n=n, kind=kind, phases=phases, case=cases,
+                                                           seed=args.seed), flush=True)
+                sys.exit(1)
+            ok = (np.array_equal(c.row_ptr, ref.row_ptr) and np.array_equal(c.col_idx[: c.nnz], ref.col_idx)
+                  and np.array_equal(np.asarray(c.values[: c.nnz]).astype(dt), ref.values)
+                  and st.generated_flops == ref.generated_flops)
+            checks += 1
+            if not ok:
+                print("MISMATCH(bt)", dict(m=m, k=k, n=n, kind=kind, phases=phases, case=cases, seed=args.seed,
+                                           got_nnz=c.nnz, ref_nnz=int(ref.row_ptr[-1])), flush=True)
+                sys.exit(1)
     cases += 1
     if args.only_case >= 0 and cases > args.only_case:
         break
