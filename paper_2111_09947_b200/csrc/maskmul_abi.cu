@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/maskmul_b200.h"
@@ -95,7 +96,8 @@ int fail(int code, const std::string& msg) {
     do {                                                                                  \
         cudaError_t _e = (call);                                                          \
         if (_e != cudaSuccess)                                                            \
-            return fail(MM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+            return fail(MM_ERR_CUDA, std::string(#call) + " (maskmul_abi.cu:" + std::to_string(__LINE__) + \
+                                         "): " + cudaGetErrorString(_e));                 \
     } while (0)
 
 // Small synchronous readback of n int64 words through the pinned scratch.
@@ -118,6 +120,12 @@ int read_i64(const void* dptr, int64_t* out, cudaStream_t st) { return read_i64s
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
+        // An error some earlier runtime call of this thread left unread (the
+        // caller's, or another library's) is not this call's: the launches below
+        // check cudaGetLastError() and would report it as their own.
+        const cudaError_t stale = cudaGetLastError();
+        if (stale != cudaSuccess && debug_launches())
+            fprintf(stderr, "[mm] stale CUDA error at entry: %s\n", cudaGetErrorString(stale));
         int cur = -1;
         if (dev < 0 || cudaGetDevice(&cur) != cudaSuccess || cur == dev) return;
         if (cudaSetDevice(dev) == cudaSuccess) prev = cur;
@@ -347,28 +355,33 @@ struct OccEntry {
     size_t smem;
     int occ;
 };
-thread_local std::vector<OccEntry> g_occ_cache;
+std::vector<OccEntry> g_occ_cache;
 struct SmemAttr {
     int device;
     const void* fn;
     size_t bytes;
 };
-thread_local std::vector<SmemAttr> g_smem_attr;
+std::vector<SmemAttr> g_smem_attr;
+std::mutex g_attr_mu;
 
 // Keyed by device as well: cudaFuncSetAttribute applies to the current
 // device's context only, so a thread that multiplies on two GPUs sets it on each.
+// The caches are process-wide (one mutex): the attribute belongs to the
+// context, not the thread — a per-thread record let a second thread lower the
+// limit under a thread that had raised it, whose next launch was then refused.
 int kernel_occupancy(const void* fn, int threads, size_t smem, int* occ) {
     int dev = 0;
     CU(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_attr_mu);
     for (const OccEntry& e : g_occ_cache)
         if (e.device == dev && e.fn == fn && e.threads == threads && e.smem == smem) { *occ = e.occ; return MM_OK; }
-    size_t* have = nullptr;
-    for (auto& a : g_smem_attr)
-        if (a.device == dev && a.fn == fn) have = &a.bytes;
-    if (!have) { g_smem_attr.push_back({dev, fn, 0}); have = &g_smem_attr.back().bytes; }
-    if (smem > *have) {
+    size_t have_i = g_smem_attr.size();
+    for (size_t q = 0; q < g_smem_attr.size(); q++)
+        if (g_smem_attr[q].device == dev && g_smem_attr[q].fn == fn) have_i = q;
+    if (have_i == g_smem_attr.size()) g_smem_attr.push_back({dev, fn, 0});
+    if (smem > g_smem_attr[have_i].bytes) {
         CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        *have = smem;
+        g_smem_attr[have_i].bytes = smem;
     }
     int o = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
@@ -376,6 +389,28 @@ int kernel_occupancy(const void* fn, int threads, size_t smem, int* occ) {
     *occ = o;
     return MM_OK;
 }
+
+// A refused launch reported with the shape it was refused at and the kernel's
+// shared-memory attributes (static bytes, the dynamic limit in force).
+int check_launch(const void* fn, int grid, int threads, size_t smem, int line) {
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return MM_OK;
+    cudaFuncAttributes fa{};
+    const cudaError_t ea = cudaFuncGetAttributes(&fa, fn);
+    cudaGetLastError();
+    std::string msg = std::string("kernel launch (maskmul_abi.cu:") + std::to_string(line) + "): " +
+                      cudaGetErrorString(e) + " [grid " + std::to_string(grid) + " threads " +
+                      std::to_string(threads) + " dynamic smem " + std::to_string(smem);
+    if (ea == cudaSuccess)
+        msg += " static smem " + std::to_string(fa.sharedSizeBytes) + " dynamic limit " +
+               std::to_string(fa.maxDynamicSharedSizeBytes) + " regs " + std::to_string(fa.numRegs);
+    return fail(MM_ERR_CUDA, msg + "]");
+}
+#define CHECK_LAUNCH(fn, grid, threads, smem)                                                    \
+    do {                                                                                         \
+        int _rc = check_launch((const void*)(fn), (grid), (threads), (smem), __LINE__);          \
+        if (_rc) return _rc;                                                                     \
+    } while (0)
 
 typedef void (*HashKernel)(Prob, Out, Work, const int8_t*, int, unsigned char*);
 
@@ -620,7 +655,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
                 fprintf(stderr, "[mm] hash bin %d rows %d gw %d threads %d cap_lg %d smem %zu grid %d occ %d\n", b,
                         cnt, gw, threads, cap_lg, smem, grid, occ);
             kern<<<grid, threads, smem, st>>>(pq, out, wk, h->row_cap_lg, cap_lg, gslab);
-            CU(cudaGetLastError());
+            CHECK_LAUNCH(kern, grid, threads, smem);
             continue;
         }
         if (is_msa_bin(b) || is_mca_bin(b)) {
@@ -652,7 +687,7 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
                 fprintf(stderr, "[mm] rank bin %d rows %d gw %d threads %d words %d nm %d smem %zu grid %d occ %d\n", b,
                         cnt, gw, threads, words_max, nm_max, smem, grid, occ);
             kern<<<grid, threads, smem, st>>>(h->prob, out, wk, words_max, nm_max, gslab);
-            CU(cudaGetLastError());
+            CHECK_LAUNCH(kern, grid, threads, smem);
             continue;
         }
         if (b == BIN_MSAW) {

@@ -92,14 +92,7 @@ def _rand_rows(rng, rows, cols, lens, dtype):
     return from_arrays(rows, cols, r, c, v)
 
 
-def test_symbolic_pass_of_float64_multiply_with_global_tier_rows():
-    """Found by tools/fuzz_gpu.py: a float64 plain multiply whose mask rows need the
-    global hash tier (29,654 entries) ran its two-phase symbolic pass (kind 0) as
-    sliced rows over tables sized for the global tier and failed; the tier is
-    decided by the multiply's kind.  Reference: two-phase driver, multiply.py:358-380."""
-    import numpy as np
-    import oracle
-    from paper_2111_09947_b200 import MultiplyPlan, arithmetic_semiring, masked_multiply_with_stats
+def _global_tier_problem():
     rng = np.random.default_rng(5)
     m, k, n = 1000, 50, 300000
     a = _rand_rows(rng, m, k, rng.integers(0, 4, m), np.float64)
@@ -107,6 +100,17 @@ def test_symbolic_pass_of_float64_multiply_with_global_tier_rows():
     mlen = rng.integers(0, 40, m)
     mlen[[3, 500]] = [29654, 12000]
     mask = _rand_rows(rng, m, n, mlen, np.int64).pattern()
+    return mask, a, b
+
+
+def test_symbolic_pass_of_float64_multiply_with_global_tier_rows():
+    """Found by tools/fuzz_gpu.py: a float64 plain multiply whose mask rows need the
+    global hash tier (29,654 entries) ran its two-phase symbolic pass (kind 0) as
+    sliced rows over tables sized for the global tier and failed; the tier is
+    decided by the multiply's kind.  Reference: two-phase driver, multiply.py:358-380."""
+    import oracle
+    from paper_2111_09947_b200 import masked_multiply_with_stats
+    mask, a, b = _global_tier_problem()
     ref = oracle.masked_multiply(mask, a, b, algorithm="msa", dtype=np.float64)
     for algo in ("auto", "hash", "msa"):
         for phases in ("1p", "2p"):
@@ -142,3 +146,49 @@ def test_direct_pass_leaves_leading_rows_to_the_binned_pass():
         assert np.array_equal(c.col_idx[: c.nnz], ref.col_idx)
         assert np.array_equal(c.values[: c.nnz], ref.values)
         assert (st.generated_flops, st.evaluated_multiplies) == (ref.generated_flops, ref.evaluated_multiplies)
+
+
+def test_second_thread_does_not_lower_a_kernels_shared_memory_limit():
+    """The dynamic shared-memory limit of a kernel belongs to the CUDA context.  The
+    library kept its record of it per thread: a second thread running the same
+    kernel at a smaller size set the limit down, and the first thread's next launch
+    at its own (recorded) size was refused with "invalid argument" (seen in the full
+    GPU suite, after the threaded parity test).  The record is process-wide now."""
+    import threading
+    import oracle
+    from paper_2111_09947_b200 import masked_multiply_with_stats
+    sem = arithmetic_semiring(np.float64)
+    mask, a, b = _global_tier_problem()
+    ref = oracle.masked_multiply(mask, a, b, algorithm="msa", dtype=np.float64)
+    plans = [MultiplyPlan(algorithm=al, phases=ph, semiring=sem) for al in ("msa", "hash", "mca") for ph in ("1p", "2p")]
+
+    def big():
+        for plan in plans:
+            c, _ = masked_multiply_with_stats(mask, a, b, plan)
+            assert np.array_equal(c.row_ptr, ref.row_ptr), plan.label()
+            assert np.array_equal(c.col_idx[: c.nnz], ref.col_idx), plan.label()
+            assert np.array_equal(c.values[: c.nnz], ref.values), plan.label()
+
+    errors = []
+
+    def small():
+        try:
+            rng = np.random.default_rng(7)
+            for n in (300, 2000, 20000, 300000):
+                sa = _rand_rows(rng, 600, 40, rng.integers(0, 4, 600), np.float64)
+                sb = _rand_rows(rng, 40, n, rng.integers(5, 30, 40), np.float64)
+                sm = _rand_rows(rng, 600, n, rng.integers(0, 6, 600), np.int64).pattern()
+                want = oracle.masked_multiply(sm, sa, sb, algorithm="msa", dtype=np.float64)
+                for plan in plans:
+                    c, _ = masked_multiply_with_stats(sm, sa, sb, plan)
+                    assert np.array_equal(c.row_ptr, want.row_ptr), (n, plan.label())
+                    assert np.array_equal(c.values[: c.nnz], want.values), (n, plan.label())
+        except BaseException as e:   # noqa: BLE001
+            errors.append(e)
+
+    big()
+    t = threading.Thread(target=small)
+    t.start()
+    t.join()
+    assert not errors, errors
+    big()
