@@ -24,6 +24,12 @@ struct Prob {
     const void* bt_val;
     const int64_t* row_flops;
     int64_t cursor_stride;   // sliced hub rows: int64 slice cursors per group (entries), 0 = none
+    // k-blocked passes of a hash bin (B larger than L2): this launch takes only the A
+    // entries whose B row starts in entries [kb_lo, kb_hi) of B; kb_pass 0 = off,
+    // 1 = first pass (stores the partial counts), 2 = middle (adds), 3 = last (adds, gathers)
+    int64_t kb_lo, kb_hi;
+    int64_t kb_min_flops;   // rows under this many products run whole in the last pass
+    int kb_pass;
     int64_t nrows;
     int64_t ncols;
 };

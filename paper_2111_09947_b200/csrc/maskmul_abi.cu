@@ -211,6 +211,13 @@ struct mm_handle {
     bool compacted = false;
     bool blen_on = true;                                // analysis gathers int32 row lengths of B (k_row_len)
     int64_t mask_nnz = 0;
+    int64_t b_nnz = 0;
+    // k-blocked passes of the 16-warp plain hash bins (one-phase, int64 / plus-pair counts):
+    // when B's index array exceeds this many bytes, the bin's launch is repeated over
+    // blocks of B of about this size, so the rows in flight share an L2-resident block
+    // (0 = off)
+    int64_t kblock_bytes = 0;
+    int64_t kblock_min_flops = 1 << 20;   // lighter rows are not cut into passes
     // ---- fused tail (fused_tail.cuh): one-launch small plain 1P multiplies ----
     unsigned* d_done = nullptr;          // device ticket counter, zero between multiplies
     TailResult* h_tail = nullptr;        // mapped pinned host memory the last block writes
@@ -650,12 +657,41 @@ int launch_bins_on(mm_handle* h, bool numeric, const Out& out, const int* order,
                 CU(cudaMallocAsync((void**)&gslab, (size_t)grid * groups * pq.cursor_stride * 8, st));
                 h->allocs.push_back(gslab);
             }
-            ++g_launches;
+            // k-blocked passes (push_hash.cuh): B's index array against L2
+            int passes = 1;
+            if (numeric && kind == 0 && mode == MODE_PLAIN && tier == 2 && !sliced && h->plan.phases == 1 &&
+                !h->plan.complemented && h->kblock_bytes > 0 && 4 * h->b_nnz > h->kblock_bytes + h->kblock_bytes / 2)
+                passes = (int)std::min<int64_t>(64, (4 * h->b_nnz + h->kblock_bytes - 1) / h->kblock_bytes);
             if (debug_launches())
-                fprintf(stderr, "[mm] hash bin %d rows %d gw %d threads %d cap_lg %d smem %zu grid %d occ %d\n", b,
-                        cnt, gw, threads, cap_lg, smem, grid, occ);
-            kern<<<grid, threads, smem, st>>>(pq, out, wk, h->row_cap_lg, cap_lg, gslab);
-            CHECK_LAUNCH(kern, grid, threads, smem);
+                fprintf(stderr, "[mm] hash bin %d rows %d gw %d threads %d cap_lg %d smem %zu grid %d occ %d passes %d\n",
+                        b, cnt, gw, threads, cap_lg, smem, grid, occ, passes);
+            Work wk_heavy = wk;
+            if (passes > 1) {
+                // the passes before the last fetch only the rows they cut
+                int32_t* list = nullptr;
+                CU(cudaMallocAsync((void**)&list, ((size_t)cnt + 1) * sizeof(int32_t), st));
+                h->allocs.push_back(list);
+                CU(cudaMemsetAsync(list, 0xff, (size_t)cnt * sizeof(int32_t), st));
+                CU(cudaMemsetAsync(list + cnt, 0, sizeof(int32_t), st));
+                ++g_launches;
+                const int sg = std::max(1, std::min((cnt + 255) / 256, h->num_sms * 8));
+                k_kb_select<<<sg, 256, 0, st>>>(h->prob, wk, (int64_t)MM_SLICE_EIGHTHS << (cap_lg - 3),
+                                                h->kblock_min_flops, list, list + cnt);
+                CU(cudaGetLastError());
+                wk_heavy.rows = list;
+            }
+            for (int ps = 0; ps < passes; ps++) {
+                if (passes > 1) {
+                    pq.kb_pass = ps == 0 ? 1 : (ps == passes - 1 ? 3 : 2);
+                    pq.kb_min_flops = h->kblock_min_flops;
+                    pq.kb_lo = h->b_nnz / passes * ps;
+                    pq.kb_hi = h->b_nnz / passes * (ps + 1);
+                    if (ps) CU(cudaMemsetAsync(wk.cursor, 0, sizeof(int32_t), st));   // the bin's row fetch restarts
+                }
+                ++g_launches;
+                kern<<<grid, threads, smem, st>>>(pq, out, ps + 1 < passes ? wk_heavy : wk, h->row_cap_lg, cap_lg, gslab);
+                CHECK_LAUNCH(kern, grid, threads, smem);
+            }
             continue;
         }
         if (is_msa_bin(b) || is_mca_bin(b)) {
@@ -1049,6 +1085,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     const bool need_bound = comp && plan->phases == 1 && !symbolic_only;
     const bool plain_1p = !comp && plan->phases == 1 && !symbolic_only;
     h->mask_nnz = mask->nnz;
+    h->b_nnz = b->nnz;
     const int64_t scan_elems = scan_scratch_elems(m);
     size_t off = 0;
     auto carve = [&](size_t bytes) { size_t at = off; off += (bytes + 255) & ~(size_t)255; return at; };
@@ -1649,6 +1686,8 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 17 && params[17] >= 0) h->fused_rows = params[17];  // 0 disables the one-launch path (fused_tail.cuh)
     if (n > 18 && params[18] >= 0) h->fused_nnz = params[18];
     if (n > 19 && params[19] >= 0) h->blen_on = params[19] != 0;
+    if (n > 20 && params[20] >= 0) h->kblock_bytes = params[20];
+    if (n > 21 && params[21] >= 0) h->kblock_min_flops = params[21];
     return MM_OK;
 }
 

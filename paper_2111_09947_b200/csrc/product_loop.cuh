@@ -115,6 +115,7 @@ struct RowFetcher {
             group_bar(bar_id, GW * 32);
             if (r >= wk.count) return false;
             ri.i = wk.rows ? wk.rows[r] : r;
+            if (ri.i < 0) return false;   // a compacted list shorter than its capacity ends with -1 (k_kb_select)
             ri.as = p.a_ptr[ri.i];
             ri.ae = p.a_ptr[ri.i + 1];
             ri.ms = p.m_ptr[ri.i];

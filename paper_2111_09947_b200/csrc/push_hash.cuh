@@ -446,7 +446,7 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
                                          int64_t ms, int64_t me, int32_t c_lo, int32_t c_hi, int64_t w_base,
                                          int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
                                          BatchSmem bsm, unsigned char* wq, uint32_t dummy_s,
-                                         unsigned long long& evaluated, int64_t* cur = nullptr) {
+                                         unsigned long long& evaluated, int64_t* cur = nullptr, int kb = 0) {
     constexpr int GT = GW * 32;
     // Plain masks in shared memory keep the table clean between rows (each
     // row cleans what it touched) and first look for a multiplier that puts
@@ -630,20 +630,32 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
             bool set = false;
             int32_t j = 0;
             int h = 0;
+            long long c = 0;
             if (t < me) {
                 j = p.m_idx[t];
                 h = CLEAN ? pl.slot(tb.keys, j) : probe_find(tb.keys, j, cap_lg, cmask);
-                set = tb.cnt[h] > 0;
+                c = tb.cnt[h];
                 if (CLEAN && KIND == 0 && NUMERIC && pl.hm != 0) evaluated += (unsigned)tb.cnt[h];
+                if (CLEAN && KIND == 0 && NUMERIC && kb) {
+                    // k-blocked passes: the row's partial counts wait in its own
+                    // (mask-shaped) value slots; the last pass reads a chunk's slots
+                    // before the prefix barrier and writes at or below them
+                    long long* acc = (long long*)o.val + w + (t - ms);
+                    if (kb == 1) *acc = c;
+                    else if (kb == 2) { if (c) *acc += c; }
+                    else c += *acc;
+                }
+                set = c > 0;
             }
+            if (CLEAN && KIND == 0 && NUMERIC && (kb == 1 || kb == 2)) continue;
             int tot;
             int pos = group_prefix<GW>(set, &tot, s_warp, bar_id, gt);
             if (NUMERIC && set) {
                 int64_t d = w + running + pos;
                 o.idx[d] = j;
                 if (KIND == 0) {
-                    if (o.out_f64) ((double*)o.val)[d] = (double)tb.cnt[h];
-                    else ((long long*)o.val)[d] = tb.cnt[h];
+                    if (o.out_f64) ((double*)o.val)[d] = (double)c;
+                    else ((long long*)o.val)[d] = c;
                 } else {
                     ((unsigned long long*)o.val)[d] = tb.val[h];
                 }
@@ -736,6 +748,39 @@ __device__ __forceinline__ int hash_part(const Prob& p, const Out& o, Table<KIND
     return running;
 }
 
+// Rows of a bin that the k-blocked passes cut (not sliced, at least min_flops
+// products), compacted to the front of `list` (filled with -1 beforehand: the row
+// fetch stops at the first); the same rule as k_push_hash's.
+__global__ void __launch_bounds__(256) k_kb_select(Prob p, Work wk, int64_t slice, int64_t min_flops,
+                                                   int32_t* list, int32_t* count) {
+    const int lane = threadIdx.x & 31;
+    for (int base = blockIdx.x * blockDim.x; base < wk.count; base += gridDim.x * blockDim.x) {
+        const int q = base + threadIdx.x;
+        int32_t i = -1;
+        bool take = false;
+        if (q < wk.count) {
+            i = wk.rows[q];
+            take = p.m_ptr[i + 1] - p.m_ptr[i] <= slice && p.row_flops[i] >= min_flops;
+        }
+        const unsigned pick = __ballot_sync(FULL, take);
+        int start = 0;
+        if (lane == 0 && pick) start = atomicAdd(count, __popc(pick));
+        start = __shfl_sync(FULL, start, 0);
+        if (take) list[start + __popc(pick & ((1u << lane) - 1))] = i;
+    }
+}
+
+// First A entry of [as, ae) whose B row starts at or after entry `bound` of B
+// (A's columns ascend, so B's row starts do): the cut of a k-blocked pass.
+__device__ __forceinline__ int64_t kb_lower(const Prob& p, int64_t as, int64_t ae, int64_t bound) {
+    while (as < ae) {
+        const int64_t mid = (as + ae) >> 1;
+        if (p.b_ptr[p.a_idx[mid]] < bound) as = mid + 1;
+        else ae = mid;
+    }
+    return as;
+}
+
 // A row.  Plain rows whose mask does not fit the largest shared table
 // (cfg5 hubs: up to 163,558 mask entries; the bin's tier-3 launch, see
 // maskmul_abi.cu) are processed in slices of 3/8 of the table's slots of
@@ -748,7 +793,7 @@ template <int GW, int KIND, int MODE, bool NUMERIC, bool SMEM>
 __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND> tb, const RowInfo& ri,
                                          int cap_lg, int cap_lg_max, int gt, int bar_id, int* s_warp,
                                          BatchSmem bsm, unsigned char* wq, uint32_t dummy_s,
-                                         unsigned long long& evaluated, int64_t* cur = nullptr) {
+                                         unsigned long long& evaluated, int64_t* cur = nullptr, int kb = 0) {
     constexpr bool CLEAN = MODE == MODE_PLAIN && SMEM && KIND != 2;
     const int64_t nm = ri.me - ri.ms;
     const int64_t w = NUMERIC ? o.off[ri.i] : 0;
@@ -761,7 +806,8 @@ __device__ __forceinline__ void hash_row(const Prob& p, const Out& o, Table<KIND
     if (!CLEAN || nm <= slice) {
         total = hash_part<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, ri.ms, ri.me, INT32_MIN, INT32_MAX, w,
                                                          cap_lg, cap_lg_max, gt, bar_id, s_warp, bsm, wq,
-                                                         dummy_s, evaluated);
+                                                         dummy_s, evaluated, nullptr, kb);
+        if (kb == 1 || kb == 2) return;   // partial counts only
     } else {
         for (int64_t s0 = ri.ms; s0 < ri.me; s0 += slice) {
             const int64_t s1 = s0 + slice < ri.me ? s0 + slice : ri.me;
@@ -850,9 +896,25 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
                 continue;
             }
         }
+        int kb = 0;
+        if (GW == 16 && MODE == MODE_PLAIN && SMEM && KIND == 0 && NUMERIC && p.kb_pass) {
+            // k-blocked passes (launch_bins_on): this launch folds only the A entries whose
+            // B row lies in the pass's block of B, so the rows in flight share an
+            // L2-resident part of B.  A row cut into slices, or too light to pay for the
+            // passes' table set-ups, runs whole in the last pass.
+            kb = p.kb_pass;
+            if (ri.me - ri.ms > ((int64_t)MM_SLICE_EIGHTHS << (cap_lg_max - 3)) || p.row_flops[ri.i] < p.kb_min_flops) {
+                if (kb != 3) continue;
+                kb = 0;
+            } else {
+                if (kb != 1) ri.as = kb_lower(p, ri.as, ri.ae, p.kb_lo);
+                if (kb != 3) ri.ae = kb_lower(p, ri.as, ri.ae, p.kb_hi);
+                if (kb == 2 && ri.as == ri.ae) continue;
+            }
+        }
         hash_row<GW, KIND, MODE, NUMERIC, SMEM>(p, o, tb, ri, row_cap_lg ? row_cap_lg[ri.i] : cap_lg_max,
                                                 cap_lg_max, gt, bar_id, s_warp + g * GW, bsm, wq, dummy_s,
-                                                evaluated, cursors);
+                                                evaluated, cursors, kb);
     }
     if (NUMERIC) {
         long long e = warp_sum_ll((long long)evaluated);

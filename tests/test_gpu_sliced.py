@@ -87,3 +87,67 @@ def test_sliced_items_match_oracle_and_sequential_slices(spec):
                             assert last_kernel_rows().get("hash_plain_t3g", 0) > 0
     finally:
         _split(True)
+
+
+def _tune(**kw):
+    """mm_set_tuning by parameter index (-1 = keep)."""
+    n = 21
+    prm = [-1] * n
+    for k, v in kw.items():
+        prm[int(k[1:])] = int(v)
+    assert _lib.load().mm_set_tuning(_handle(torch.cuda.current_device()), (C.c_int64 * n)(*prm), n) == 0
+
+
+def _launches_of(fn):
+    lib = _lib.load()
+    h = _handle(torch.cuda.current_device())
+    lib.mm_profile_enable(h, 1)
+    try:
+        out = fn()
+        ms = (C.c_float * 6)()
+        n = C.c_int64(0)
+        lib.mm_profile_read(h, ms, 6, C.byref(n))
+    finally:
+        lib.mm_profile_enable(h, 0)
+    return out, int(n.value)
+
+
+def test_kblocked_passes_match_oracle():
+    """k-blocked passes of the 16-warp plain hash bins (push_hash.cuh, launch_bins_on):
+    when B's index array is larger than the block size, the bin's launch is repeated
+    over blocks of B's rows and the partial counts wait in the row's mask-shaped
+    output slots.  One-phase plus-pair results (int64 and float64 outputs) must equal
+    the C oracle bit for bit at every block size, rows without A entries in some blocks
+    and rows cut into slices included; the plans the blocking does not apply to
+    (two-phase, plus-times) are unchanged.  Reference semantics: hash_numeric
+    (_kernels.py:130-218)."""
+    a, b, m = _hub_problem(21, 120, 60_000, 300, 9000, 500, empty_rows=(5,))
+    # half of the rows meet only the first third of B's rows: no A entry in the later blocks
+    rows_of = np.repeat(np.arange(a.nrows), np.diff(a.row_ptr))
+    keep = ~((rows_of % 2 == 1) & (a.col_idx >= 1000))
+    a = from_arrays(a.nrows, a.ncols, rows_of[keep], a.col_idx[keep], np.asarray(a.values)[keep])
+    b_bytes = 4 * b.nnz
+    try:
+        for sem in (plus_pair_semiring(np.int64), plus_pair_semiring(np.float64), arithmetic_semiring(np.int64)):
+            r = oracle.masked_multiply(m.pattern(), a, b, semiring_id=sem.kernel_id, dtype=sem.dtype)
+            want = digest_csr(r.row_ptr, r.col_idx, r.values)
+            for algo in ("hash", "auto"):
+                for ph in ("1p", "2p"):
+                    plan = MultiplyPlan(algorithm=algo, phases=ph, semiring=sem)
+                    _tune(p20=0)
+                    (c0, st0), n0 = _launches_of(lambda: masked_multiply_with_stats(m.pattern(), a, b, plan))
+                    assert digest_csr(c0.row_ptr, c0.col_idx, c0.values) == want
+                    for blocks in (2, 3, 7):
+                        _tune(p20=b_bytes // blocks + 4)
+                        (c, st), n = _launches_of(lambda: masked_multiply_with_stats(m.pattern(), a, b, plan))
+                        assert digest_csr(c.row_ptr, c.col_idx, c.values) == want, (sem.name, algo, ph, blocks)
+                        assert st.evaluated_multiplies == r.evaluated_multiplies, (sem.name, algo, ph, blocks)
+                        assert st.generated_flops == r.generated_flops
+                        blocked = ph == "1p" and sem.kernel_id != 0
+                        if blocked and algo == "hash":
+                            assert last_kernel_rows().get("hash_plain_t2s", 0) + last_kernel_rows().get("hash_plain_t2l", 0) > 0
+                            assert n > n0, (sem.name, algo, ph, blocks, n, n0)     # the bin's launch repeated
+                        if not blocked:
+                            assert n == n0
+    finally:
+        _tune(p20=0)
