@@ -174,7 +174,11 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
  * smallest plain one-phase multiplies (8192 / 2^17; 0 disables it): the row
  * kernel's last block scans, compacts and reports through mapped host memory,
  * params[19] = 0 makes the analysis gather B's 8-byte row offsets instead of
- * the int32 row lengths it otherwise derives first. */
+ * the int32 row lengths it otherwise derives first,
+ * params[20] = k-blocked passes of the 16-warp plain hash bins of one-phase
+ * plus-pair multiplies: bytes of B's index array per block of B's rows (0 =
+ * off, the default: measured slower on cfg5), params[21] = rows
+ * under this many products are not cut into passes (2^20). */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

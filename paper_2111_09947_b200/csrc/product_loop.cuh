@@ -77,7 +77,9 @@ struct RowInfo {
 #ifndef MM_ROWS_PER_FETCH
 #define MM_ROWS_PER_FETCH 4
 #endif
-template <int GW>
+// ENDMARK: the row list may be shorter than wk.count and then ends with -1
+// (k_kb_select's compacted list, push_hash.cuh)
+template <int GW, bool ENDMARK = false>
 struct RowFetcher {
     int n = 0, q = 0;
     int per = MM_ROWS_PER_FETCH;   // rows per fetch (1-warp groups); 1 when rows are few per warp
@@ -115,7 +117,7 @@ struct RowFetcher {
             group_bar(bar_id, GW * 32);
             if (r >= wk.count) return false;
             ri.i = wk.rows ? wk.rows[r] : r;
-            if (ri.i < 0) return false;   // a compacted list shorter than its capacity ends with -1 (k_kb_select)
+            if (ENDMARK && ri.i < 0) return false;
             ri.as = p.a_ptr[ri.i];
             ri.ae = p.a_ptr[ri.i + 1];
             ri.ms = p.m_ptr[ri.i];

@@ -876,7 +876,7 @@ k_push_hash(Prob p, Out o, Work wk, const int8_t* row_cap_lg, int cap_lg_max,
         group_bar(bar_id, GT);
     }
     unsigned long long evaluated = 0;
-    RowFetcher<GW> rf;
+    RowFetcher<GW, GW == 16 && MODE == MODE_PLAIN && SMEM && KIND == 0 && NUMERIC> rf;
     if (wk.count < 4 * (int)(gridDim.x * groups)) rf.per = 1;   // few rows per group: one per fetch
     RowInfo ri;
     while (rf.next(p, wk, gt, bar_id, s_row + g, ri)) {

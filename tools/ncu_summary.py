@@ -40,6 +40,12 @@ KEYS = [
 
 def main(path, pattern=""):
     rows = list(csv.reader(open(path)))
+    # ncu's own ==PROF== / ==WARNING== lines (and anything the profiled program
+    # printed) come before the CSV header when stdout was captured whole
+    while rows and "Kernel Name" not in rows[0]:
+        rows.pop(0)
+    if len(rows) < 2:
+        sys.exit(f"{path}: no ncu raw-page CSV header found")
     hdr = rows[0]
     units = rows[1]
     col = {h: i for i, h in enumerate(hdr)}
