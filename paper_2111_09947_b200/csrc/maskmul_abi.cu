@@ -518,6 +518,9 @@ int launch_bins(mm_handle* h, bool numeric, const Out& out) {
 // (push_hash_items.cuh): item list, the items kernel, the join.
 int launch_slice_items(mm_handle* h, const Out& out, const Work& wk, int kind, int cap_lg, size_t smem,
                        cudaStream_t st) {
+    if (ITEM_GW != 16)   // the caller sized the 16-warp tier's block: one table, this kernel's batch and queues
+        smem = ((size_t)1 << cap_lg) * (kind == 0 ? 8 : 16) + batch_bytes_rt(ITEM_GW, kind) +
+               (size_t)ITEM_GW * 64 * (kind == 1 ? 24 : 8);
     const int64_t slice = (int64_t)MM_SLICE_EIGHTHS << (cap_lg - 3);
     const int64_t max_items = (int64_t)wk.count + (h->mask_nnz + slice - 1) / slice;
     if (max_items >= (1ll << 31)) return fail(MM_ERR_INTERNAL, "too many slice items");

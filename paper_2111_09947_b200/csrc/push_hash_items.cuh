@@ -19,7 +19,10 @@
 
 namespace mm {
 
-constexpr int ITEM_GW = 16;
+#ifndef MM_ITEM_GW
+#define MM_ITEM_GW 32
+#endif
+constexpr int ITEM_GW = MM_ITEM_GW;   // 32 warps: one 1024-thread block per SM at 64 registers (16: cfg5 349.6 vs 334.4 ms)
 
 // One block: block-wide exclusive scan of x over 1024 threads; returns the
 // thread's offset and the total in *tot.
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(1024) k_slice_items(Prob p, Work wk, int64_t s
 
 // Groups of ITEM_GW warps fetch (row, slice) items; table in shared memory.
 template <int KIND>
-__global__ void __launch_bounds__(ITEM_GW * 32, MM_HASH16_MINB)
+__global__ void __launch_bounds__(ITEM_GW * 32, ITEM_GW == 32 ? 1 : MM_HASH16_MINB)
 k_push_hash_items(Prob p, Out o, Work wk, const int32_t* item_q, const int32_t* item_s, const int32_t* n_items,
                   int32_t* item_cursor, int64_t slice, int cap_lg_max, const int32_t* row_base,
                   int32_t* slice_cnt) {

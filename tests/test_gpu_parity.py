@@ -312,6 +312,17 @@ def test_cfg3_bitwise(d):
     gold = load_npz(f"cfg3_d{d}_C.npz")
     rel = np.abs(c.values - gold["values"]) / np.maximum(np.abs(gold["values"]), 1e-300)
     assert rel.max(initial=0) <= 1e-12
+    # the heap family and the two-phase push plans on the same inputs: pattern bit-exact,
+    # float64 values within the north_star's 1e-12 relative (the heap folds in ascending k,
+    # the reference's in heap-pop order, _kernels.py:380-463)
+    for algo, ph in (("heap", "1p"), ("heapdot", "1p"), ("heap", "2p"), ("msa", "2p"), ("hash", "2p"), ("auto", "2p")):
+        c, st = masked_multiply_with_stats(w.mask, w.a, w.b, MultiplyPlan(algorithm=algo, phases=ph,
+                                                                          semiring=w.semiring))
+        assert np.array_equal(c.row_ptr, gold["row_ptr"]), (algo, ph)
+        assert np.array_equal(c.col_idx[: c.nnz], gold["col_idx"]), (algo, ph)
+        rel = np.abs(c.values[: c.nnz] - gold["values"]) / np.maximum(np.abs(gold["values"]), 1e-300)
+        assert rel.max(initial=0) <= 1e-12, (algo, ph)
+        assert st.generated_flops == g["generated"], (algo, ph)
 
 
 def test_cfg4_complement_bitwise():
