@@ -23,6 +23,15 @@
  * 3 internal bound violation (the reference's assertions at
  * multiply.py:375,390), 4 CUDA error.  mm_last_error() returns a thread-local
  * message for the last non-zero status.
+ *
+ * Threads: a handle (mm_create) serves one multiply at a time — give every
+ * host thread its own (the Python host keeps one per device and thread).
+ * Different handles may be used concurrently from different threads; what the
+ * library shares between them (its record of each kernel's occupancy and
+ * dynamic shared-memory limit, which belong to the CUDA context) sits behind
+ * one mutex.  Every entry runs on its handle's / operands' device and
+ * restores the caller's current device; an error some earlier CUDA call of
+ * the thread left unread is dropped at entry, not reported as this call's.
  */
 #ifndef MASKMUL_B200_H
 #define MASKMUL_B200_H
