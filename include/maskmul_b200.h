@@ -187,7 +187,8 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches);
  * params[20] = k-blocked passes of the 16-warp plain hash bins of one-phase
  * plus-pair multiplies: bytes of B's index array per block of B's rows (0 =
  * off, the default: measured slower on cfg5), params[21] = rows
- * under this many products are not cut into passes (2^20). */
+ * under this many products are not cut into passes (2^20), params[22] =
+ * params[1] for plain order-free hash rows (524288; params[1] sets both). */
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n);
 /* Rows and generated flops per kernel bin of the last multiply (bin ids in
  * DESIGN.md §4); returns the number of bins. */

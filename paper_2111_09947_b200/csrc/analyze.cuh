@@ -61,6 +61,10 @@ __host__ __device__ constexpr int tier_cap_lg_pair(int t) { return t == 0 ? 10 :
 __host__ __device__ constexpr int tier_cap_lg_val(int t) { return t == 0 ? 10 : (t == 1 ? 12 : (t == 2 ? 13 : 30)); }
 constexpr int64_t TIER_FLOPS0 = 8192;
 constexpr int64_t TIER_FLOPS1 = 65536;
+// Plain order-free hash rows stay in the 4-warp tier up to 8x more products (when their table
+// fits it): cfg5 334.4 -> 316.8 ms at 2^19 (326.8 at 2^17, 325.6 at 2^20, 540 at 2^22), while the
+// MSA tiers of cfg2 lose 11 % past 2^17 — hence a boundary of its own.
+constexpr int64_t TIER_FLOPS1_HASH = 524288;
 
 struct Summary {
     unsigned long long gen_flops;
@@ -81,6 +85,7 @@ struct Summary {
 struct AnalyzeParams {
     long long tier_flops0;   // rows with <= this many products: 1-warp tier
     long long tier_flops1;   // ... 4-warp tier; above: 16-warp tier
+    long long tier_flops1_hash;   // the same boundary for plain order-free hash rows (see TIER_FLOPS1_HASH)
     int capc_lg;             // table-size class boundary (log2 slots)
     int load_shift;          // preferred table size = keys << load_shift
     int load_shift_wide;     // same for plain rows of the 16-warp tier
@@ -255,7 +260,9 @@ __device__ __forceinline__ int classify_row(const AnalyzeParams& ap, int64_t na,
         }
         // a binary search per product is a chain of dependent loads: spread
         // the row's products over more lanes much earlier than for probing
-        const int tfm = mode == MODE_CSRCH ? (flops <= 64 ? 0 : (flops <= 1024 ? 1 : 2)) : tf;
+        const int tfh = mode == MODE_PLAIN && !ap.ordered
+                            ? (flops <= ap.tier_flops0 ? 0 : (flops <= ap.tier_flops1_hash ? 1 : 2)) : tf;
+        const int tfm = mode == MODE_CSRCH ? (flops <= 64 ? 0 : (flops <= 1024 ? 1 : 2)) : tfh;
         tier = tc > tfm ? tc : tfm;
     }
     // wide plain rows (16-warp tier) hold their keys by two-choice cuckoo

@@ -197,6 +197,7 @@ struct mm_handle {
     int bound_flag = 0;
     // ---- tuning (mm_set_tuning) ----
     long long tier_flops0 = TIER_FLOPS0, tier_flops1 = TIER_FLOPS1;   // defaults: analyze.cuh
+    long long tier_flops1_hash = TIER_FLOPS1_HASH;
     int capc_lg = CAPC_LG, load_shift = 2, load_shift_wide = 1;
     int rank_budget[3] = {6144, 24576, 49152};
     int auto_mca_nm = 0;
@@ -1069,6 +1070,7 @@ int begin_impl(mm_handle* h, const mm_plan_t* plan, const mm_matrix_t* mask, con
     }
     ap.tier_flops0 = h->tier_flops0;
     ap.tier_flops1 = h->tier_flops1;
+    ap.tier_flops1_hash = h->tier_flops1_hash;
     ap.capc_lg = h->capc_lg;
     ap.load_shift = h->load_shift;
     ap.load_shift_wide = h->load_shift_wide;
@@ -1672,7 +1674,7 @@ int mm_profile_read(mm_handle_t* h, float* ms, int n, int64_t* launches) {
 int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (!h) return fail(MM_ERR_INPUT, "null handle");
     if (n > 0 && params[0] > 0) h->tier_flops0 = params[0];
-    if (n > 1 && params[1] > 0) h->tier_flops1 = params[1];
+    if (n > 1 && params[1] > 0) h->tier_flops1 = h->tier_flops1_hash = params[1];   // params[22] sets the hash one apart
     if (n > 2 && params[2] > 0) h->capc_lg = (int)params[2];
     if (n > 3 && params[3] > 0 && params[3] <= 4) h->load_shift = (int)params[3];
     for (int t = 0; t < 3; t++)
@@ -1691,6 +1693,7 @@ int mm_set_tuning(mm_handle_t* h, const int64_t* params, int n) {
     if (n > 19 && params[19] >= 0) h->blen_on = params[19] != 0;
     if (n > 20 && params[20] >= 0) h->kblock_bytes = params[20];
     if (n > 21 && params[21] >= 0) h->kblock_min_flops = params[21];
+    if (n > 22 && params[22] > 0) h->tier_flops1_hash = params[22];
     return MM_OK;
 }
 
